@@ -1,0 +1,317 @@
+"""HPG-MxP bench on B200: one JSON line (driver contract).
+
+A "step" is one double-single GMRES-IR solve of the benchmark problem
+(27-point stencil, b = A 1, x0 = 0, 4-level V-cycle, restart 30, tol 1e-9,
+max 300 iterations -- the reference's timed-phase solve, ref: bench.py:189-213)
+at 256^3 rows per GPU (BASELINE.json configs[1]; weak scaling over the
+factor_ranks process grid for N > 1).  ``value`` is the HPG-MxP GFLOP/s of the
+timed mixed solves, penalised by min(1, n_d / n_ir) from a standard validation
+run at the same local size (the reference CLI's headline number,
+ref: bench.py:240-270); raw, fp64 and speedup figures ride along.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HPG-MxP GFLOP/s (mixed, and speedup vs fp64) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "GFLOP/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+
+
+# ------------------------------------------------------------------ clocks
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (profiling recipe's clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle)
+
+CPU_L = 64
+CPU_ITERS = 10
+
+
+def cpu_port_sample(iters=CPU_ITERS, L=CPU_L):
+    """The oracle port (numpy restatement of the reference) on this host: one mixed
+    GMRES-IR solve at L^3 capped at `iters` inner iterations.  Returns (gflops, seconds)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import hpgmxp_oracle as O
+    s = O.Solver(L, L, L, 1, 4)
+    b = s.rhs()
+    s.count = O.Count()
+    t0 = time.perf_counter()
+    s.gmres(b, "mixed", 1e-9, iters, 30)
+    dt = time.perf_counter() - t0
+    return sum(s.count.flops.values()) / dt / 1e9, dt
+
+
+def run_reference(args):
+    rank, world = _env_rank()
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        cpu_port_sample()
+    vals, secs = [], []
+    for _ in range(args.steps):
+        g, dt = cpu_port_sample()
+        vals.append(g)
+        secs.append(dt)
+    v = float(np.mean(vals))
+    sample = (f"{CPU_L}^3 local grid (256^3 is infeasible on the host: minutes of setup, hours "
+              f"per solve), one mixed GMRES-IR solve capped at {CPU_ITERS} inner iterations per "
+              "step, oracle port (numpy restatement of mxpbench), stencil motifs single-threaded")
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(secs)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+            "data": "synthetic (the benchmark's own generated 27-point problem)",
+            "impl": "reference",
+            "config": {"workload": "HPG-MxP double-single GMRES-IR, 4-level MG, restart 30",
+                       "local_grid": f"{CPU_L}^3 (sample)", "parallelism": "host"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args):
+    import torch
+    from paper_2507_11512_b200 import _lib
+    from paper_2507_11512_b200.bench import BenchConfig, _build_state, _solve, run_validation
+    from paper_2507_11512_b200.comm import World, runtime
+    from paper_2507_11512_b200.krylov import gmres_solve
+    from paper_2507_11512_b200.metrics import MOTIFS, Tally, penalty_factor
+
+    rank, nproc = _env_rank()
+    if nproc != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={nproc}")
+    rt = runtime()
+    world = World(nproc) if nproc > 1 else None
+    L = args.local
+    cfg = BenchConfig(local_nx=L, local_ny=L, local_nz=L, ranks=nproc, time_seconds=0,
+                      max_iters=args.max_iters)
+    peak, peak_kind = _peaks()
+
+    # validation (n_d, n_ir -> penalty), standard mode on one rank at the local size
+    val = None
+    if not args.no_validation:
+        val = run_validation(cfg, world if world is not None else World(1))
+
+    hier, lv, b = _build_state(cfg, nproc, world, rank)
+    ctx = hier.ctx
+    n = lv.A_hi.n_rows
+    stream = rt.stream
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world is not None:
+            world.barrier()
+
+    def timed(mode, steps, tally=None):
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        l0 = ctx.launches()
+        iters = []
+        e0.record(stream)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            res = _solve(cfg, hier, lv, b, world, rank, mode, cfg.tol, cfg.max_iters, tally)
+            iters.append(res.iterations)
+        e1.record(stream)
+        barrier()
+        wall = time.perf_counter() - t0
+        dev = e0.elapsed_time(e1) / 1e3
+        return dev, wall, iters, ctx.launches() - l0, res
+
+    # warm-up
+    for _ in range(args.warmup):
+        _solve(cfg, hier, lv, b, world, rank, "mixed", cfg.tol, cfg.max_iters)
+    # flops of one solve (model, this rank) -- count on a tallied solve
+    tal = Tally()
+    res = _solve(cfg, hier, lv, b, world, rank, "mixed", cfg.tol, cfg.max_iters, tal)
+    flops_rank = tal.total_flops()
+    bytes_rank = tal.total_bytes()
+    gs_bytes = tal.bytes["GS"]
+    gs_sec = tal.seconds["GS"]
+
+    clocks = Clocks(rt.device.index)
+    clocks.start()
+    dev_s, wall_s, iters, launches, last = timed("mixed", args.steps)
+    clk = clocks.stop()
+    # timing of the dominant motif (GS) inside a timed solve: library CUDA events
+    tal2 = Tally()
+    _solve(cfg, hier, lv, b, world, rank, "mixed", cfg.tol, cfg.max_iters, tal2)
+    gs_bytes, gs_sec = tal2.bytes["GS"], tal2.seconds["GS"]
+    l0_pass = ctx.gs_level0_stats() if hasattr(ctx, "gs_level0_stats") else None
+
+    # fp64 comparison (same solves in double)
+    dtal = Tally()
+    _solve(cfg, hier, lv, b, world, rank, "double", cfg.tol, cfg.max_iters, dtal)
+    dflops_rank = dtal.total_flops()
+    ddev_s, dwall_s, diters, _, _ = timed("double", args.steps)
+
+    # e2e through the public API with host buffers (H2D b, D2H x inside the region)
+    b_host = b.cpu().numpy()
+    x_host = np.zeros(n)
+    b_pin = torch.from_numpy(b_host).pin_memory().numpy()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x_host[:] = 0
+        gmres_solve(lv.A_hi, lv.A_lo, hier.preconditioner(), b_pin, x0=x_host, mode="mixed",
+                    tol=cfg.tol, max_iters=cfg.max_iters, m=cfg.restart, plan=lv.plan,
+                    world=world, rank=rank)
+    barrier()
+    e2e_s = time.perf_counter() - t0
+
+    # max over ranks, sums of flops over ranks
+    def reduce(vals, op):
+        if world is None:
+            return vals
+        parts = world.gather(rank, vals)
+        parts = world.broadcast_bytes(parts)
+        return [op(p[i] for p in parts) for i in range(len(vals))]
+
+    dev_s, ddev_s, e2e_s, wall_s = reduce([dev_s, ddev_s, e2e_s, wall_s], max)
+    flops_all, dflops_all, bytes_all = reduce([flops_rank, dflops_rank, bytes_rank], sum)
+    hier.close()
+    if rank != 0:
+        return 0
+
+    K = args.steps
+    raw = flops_all * K / dev_s / 1e9
+    penalty = penalty_factor(val["n_d"], val["n_ir"]) if val else None
+    value = raw * penalty if penalty is not None else raw
+    fp64 = dflops_all * K / ddev_s / 1e9
+    gs_gbs = gs_bytes / gs_sec / 1e9 if gs_sec > 0 else 0.0
+    cpu_g, cpu_s = cpu_port_sample() if nproc == 1 and not args.no_cpu else (None, None)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": nproc, "steps": K,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32 (double-single GMRES-IR)",
+        "data": "synthetic (the benchmark's own generated 27-point problem, b = A*1)",
+        "config": {"workload": "HPG-MxP double-single GMRES-IR solve (4-level MG V-cycle, "
+                               "multicolor GS, restart 30, tol 1e-9, max 300 it)",
+                   "local_grid": f"{L}^3 per GPU", "process_grid": list(_grid(nproc)),
+                   "parallelism": f"3D domain decomposition x{nproc}",
+                   "l2": "inputs larger than L2 (ELL operands ~7 GB per GPU)"},
+        "raw_gflops": raw, "penalty": penalty,
+        "validation": val, "iterations_per_solve": iters,
+        "fp64_gflops": fp64, "fp64_iterations_per_solve": diters,
+        "speedup_vs_fp64": value / fp64 if fp64 else None,
+        "solve_roofline": {"model_bytes_per_solve": bytes_all,
+                           "achieved_gbs": bytes_all * K / dev_s / 1e9,
+                           "peak_gbs": peak * nproc,
+                           "frac": bytes_all * K / dev_s / 1e9 / (peak * nproc)},
+        "roofline": {"bound": "hbm", "kernel": "k_gs_pass (multicolor GS, all levels, fp32)",
+                     "achieved": gs_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": gs_gbs / peak, "traffic": None,
+                     "peak_kind": peak_kind},
+        "e2e": {"value": value * dev_s / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * 8,
+                "d2h_bytes_per_step": n * 8},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "wall_seconds": wall_s,
+    }
+    if cpu_g is not None:
+        line["cpu_baseline"] = {
+            "value": cpu_g, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{CPU_L}^3, one mixed GMRES-IR solve capped at {CPU_ITERS} iterations "
+                      f"({cpu_s:.1f} s), oracle numpy port on this host"}
+    print(json.dumps(line))
+    return 0
+
+
+def _grid(n):
+    from paper_2507_11512_b200.geometry import factor_ranks
+    return factor_ranks(n)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--local", type=int, default=256)
+    p.add_argument("--max-iters", type=int, default=300)
+    p.add_argument("--no-validation", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    args = p.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

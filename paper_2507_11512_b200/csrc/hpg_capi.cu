@@ -1,0 +1,874 @@
+// libhpgmxp.so: context, hierarchy build, and the extern "C" entry points
+// declared in include/hpgmxp.h.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hpgmxp.h"
+#include "hpg_geom.h"
+#include "hpg_kernels.cuh"
+
+using hpg::Geom;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                              \
+  do {                                                                                              \
+    cudaError_t e_ = (expr);                                                                        \
+    if (e_ != cudaSuccess) return fail(HPG_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr,       \
+                                       cudaGetErrorString(e_));                                     \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                              \
+  do {                                                                                              \
+    ncclResult_t r_ = (expr);                                                                       \
+    if (r_ != ncclSuccess) return fail(HPG_E_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #expr,       \
+                                       ncclGetErrorString(r_));                                     \
+  } while (0)
+
+#define LAUNCH_CHECK()                                                                              \
+  do {                                                                                              \
+    cudaError_t e_ = cudaGetLastError();                                                            \
+    if (e_ != cudaSuccess) return fail(HPG_E_CUDA, "%s:%d launch: %s", __FILE__, __LINE__,          \
+                                       cudaGetErrorString(e_));                                     \
+  } while (0)
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------ geometry (host)
+
+int64_t nnz_axis(int l, int o, int g) {
+  int64_t s = 0;
+  for (int x = 0; x < l; ++x)
+    for (int d = -1; d <= 1; ++d) s += (o + x + d >= 0 && o + x + d < g);
+  return s;
+}
+
+Geom make_geom(const int l[3], const int c[3], const int p[3]) {
+  Geom g;
+  memset(&g, 0, sizeof g);
+  g.lx = l[0];
+  g.ly = l[1];
+  g.lz = l[2];
+  g.ox = c[0] * l[0];
+  g.oy = c[1] * l[1];
+  g.oz = c[2] * l[2];
+  g.gx = p[0] * l[0];
+  g.gy = p[1] * l[1];
+  g.gz = p[2] * l[2];
+  g.n = (int64_t)l[0] * l[1] * l[2];
+  int nact = 0;
+  for (int a = 0; a < 3; ++a) g.bit[a] = l[a] >= 2 ? nact++ : -1;
+  g.ncolors = g.n ? 1 << nact : 0;
+  g.off[0] = 0;
+  for (int col = 0; col < g.ncolors; ++col) {
+    int64_t size = 1;
+    for (int a = 0; a < 3; ++a) {
+      const int par = g.bit[a] >= 0 ? (col >> g.bit[a]) & 1 : 0;
+      size *= (l[a] - par + 1) / 2;
+    }
+    g.off[col + 1] = g.off[col] + size;
+  }
+  for (int col = g.ncolors + 1; col < 9; ++col) g.off[col] = g.n;
+  // neighbours sorted by rank id; halo slots in that order (ref: comm.py:219-227)
+  struct Nb {
+    int rank, idx;
+    int64_t cnt;
+  };
+  std::vector<Nb> nbs;
+  for (int i = 0; i < 27; ++i) {
+    g.halo_base[i] = -1;
+    g.nbr_rank[i] = -1;
+  }
+  for (int sz = -1; sz <= 1; ++sz)
+    for (int sy = -1; sy <= 1; ++sy)
+      for (int sx = -1; sx <= 1; ++sx) {
+        if (!sx && !sy && !sz) continue;
+        const int cx = c[0] + sx, cy = c[1] + sy, cz = c[2] + sz;
+        if (cx < 0 || cx >= p[0] || cy < 0 || cy >= p[1] || cz < 0 || cz >= p[2]) continue;
+        nbs.push_back({cx + p[0] * (cy + p[1] * cz), hpg::offset_index(sx, sy, sz), hpg::region_size(g, sx, sy, sz)});
+      }
+  std::sort(nbs.begin(), nbs.end(), [](const Nb& a, const Nb& b) { return a.rank < b.rank; });
+  int64_t base = g.n;
+  for (auto& nb : nbs) {
+    g.halo_base[nb.idx] = base;
+    g.nbr_rank[nb.idx] = nb.rank;
+    base += nb.cnt;
+  }
+  g.halo_size = base - g.n;
+  return g;
+}
+
+int64_t geom_nnz(const Geom& g) {
+  return nnz_axis(g.lx, g.ox, g.gx) * nnz_axis(g.ly, g.oy, g.gy) * nnz_axis(g.lz, g.oz, g.gz);
+}
+
+size_t esize(int prec) { return prec == HPG_F64 ? 8 : 4; }
+ncclDataType_t nccl_type(int prec) { return prec == HPG_F64 ? ncclFloat64 : ncclFloat32; }
+
+struct Nbr {
+  int rank;
+  int idx;
+  int64_t send_off, cnt, recv_base;
+};
+
+struct Level {
+  Geom g;
+  int64_t n = 0, n_ext = 0, ld = 0, nnz = 0;
+  int32_t* cols = nullptr;
+  double* v64 = nullptr;
+  float* v32 = nullptr;
+  int32_t* inj = nullptr;  // (coarse levels) dst[j] for fine color-0 row j
+  std::vector<Nbr> nbrs;
+  int32_t* send_idx = nullptr;
+  int64_t send_total = 0;
+  void* send_buf = nullptr;
+  double* z64 = nullptr;
+  float* z32 = nullptr;
+  double* r64 = nullptr;
+  float* r32 = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct hpg_ctx {
+  int device = 0, rank = 0, nranks = 1;
+  int procs[3] = {1, 1, 1}, coords[3] = {0, 0, 0};
+  int nlev = 0, nu1 = 1, nu2 = 1, nu_c = 1;
+  std::vector<Level> lev;
+  cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  ncclComm_t comm = nullptr;
+  int nb = 0;                   // reduction grid
+  void* partial = nullptr;      // nb * 64 elements (f64-sized)
+  double* spmv_partial = nullptr;
+  int64_t spmv_partial_len = 0;
+  void* scal = nullptr;         // 256 f64-sized device scalars
+  void* gather = nullptr;       // nranks * 256
+  double* pinned = nullptr;     // 256 host doubles
+  int64_t launches = 0;
+  // per-motif CUDA-event timers (ref: metrics.py:125-131 Tally.timed)
+  bool timing = false;
+  std::vector<cudaEvent_t> events;
+  size_t ev_used = 0;
+  std::vector<std::pair<int, size_t>> marks;  // (motif, index of start event; end = +1)
+};
+
+namespace {
+
+enum Motif { M_GS = 0, M_SPMV = 1, M_ORTHO = 2, M_RESTRICT = 3, M_PROLONG = 4, M_VEC = 5 };
+
+// RAII motif region: records an event pair on the compute stream when timing is on
+struct Timed {
+  hpg_ctx* c;
+  int motif;
+  size_t idx = (size_t)-1;
+  Timed(hpg_ctx* c_, int m) : c(c_), motif(m) {
+    if (!c->timing) return;
+    while (c->events.size() < c->ev_used + 2) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return;
+      c->events.push_back(e);
+    }
+    idx = c->ev_used;
+    c->ev_used += 2;
+    cudaEventRecord(c->events[idx], c->stream);
+  }
+  ~Timed() {
+    if (idx == (size_t)-1) return;
+    cudaEventRecord(c->events[idx + 1], c->stream);
+    c->marks.push_back({motif, idx});
+  }
+};
+
+template <typename T>
+T* vals_of(const Level& L);
+template <>
+double* vals_of<double>(const Level& L) { return L.v64; }
+template <>
+float* vals_of<float>(const Level& L) { return L.v32; }
+
+int grid_for(int64_t n, int threads = 256) { return (int)std::max<int64_t>(1, cdiv(n, threads)); }
+
+int do_exchange(hpg_ctx* c, int l, int prec, void* v) {
+  Level& L = c->lev[l];
+  if (c->nranks == 1 || L.nbrs.empty()) return HPG_OK;
+  if (L.send_total) {
+    if (prec == HPG_F64)
+      hpg::k_pack<double><<<grid_for(L.send_total), 256, 0, c->stream>>>((const double*)v, L.send_idx, L.send_total,
+                                                                         (double*)L.send_buf);
+    else
+      hpg::k_pack<float><<<grid_for(L.send_total), 256, 0, c->stream>>>((const float*)v, L.send_idx, L.send_total,
+                                                                        (float*)L.send_buf);
+    LAUNCH_CHECK();
+    ++c->launches;
+  }
+  const size_t es = esize(prec);
+  NCCL_TRY(ncclGroupStart());
+  for (auto& nb : L.nbrs) {
+    NCCL_TRY(ncclSend((char*)L.send_buf + nb.send_off * es, nb.cnt, nccl_type(prec), nb.rank, c->comm, c->stream));
+    NCCL_TRY(ncclRecv((char*)v + nb.recv_base * es, nb.cnt, nccl_type(prec), nb.rank, c->comm, c->stream));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  return HPG_OK;
+}
+
+// rank-ordered allreduce of cnt device scalars in place (ref: comm.py:97-108)
+template <typename T>
+int allreduce_scal(hpg_ctx* c, T* buf, int cnt) {
+  if (c->nranks == 1) return HPG_OK;
+  NCCL_TRY(ncclAllGather(buf, c->gather, cnt, sizeof(T) == 8 ? ncclFloat64 : ncclFloat32, c->comm, c->stream));
+  hpg::k_fold_ranks<T><<<1, 64, 0, c->stream>>>((const T*)c->gather, c->nranks, cnt, buf, 0);
+  LAUNCH_CHECK();
+  ++c->launches;
+  return HPG_OK;
+}
+
+template <typename T>
+int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
+  Timed tm(c, M_GS);
+  Level& L = c->lev[l];
+  if (zero) {
+    CUDA_TRY(cudaMemsetAsync(z, 0, L.n_ext * sizeof(T), c->stream));
+  } else {
+    int rc = do_exchange(c, l, sizeof(T) == 8 ? HPG_F64 : HPG_F32, z);
+    if (rc) return rc;
+  }
+  const T* vals = vals_of<T>(L);
+  for (int col = 0; col < L.g.ncolors; ++col) {
+    const int64_t a = L.g.off[col], b = L.g.off[col + 1];
+    if (b <= a) continue;
+    hpg::k_gs_pass<T><<<grid_for(b - a), 256, 0, c->stream>>>(L.cols, vals, L.ld, a, b - a, r, z);
+    LAUNCH_CHECK();
+    ++c->launches;
+  }
+  return HPG_OK;
+}
+
+template <typename T>
+int restrict_(hpg_ctx* c, int l, const T* rf, const T* zf, T* rcoarse) {
+  Timed tm(c, M_RESTRICT);
+  Level& F = c->lev[l];
+  Level& C = c->lev[l + 1];
+  hpg::k_restrict<T><<<grid_for(C.n), 256, 0, c->stream>>>(F.cols, vals_of<T>(F), F.ld, C.n, C.inj, rf, zf, rcoarse);
+  LAUNCH_CHECK();
+  ++c->launches;
+  return HPG_OK;
+}
+
+template <typename T>
+int prolong_(hpg_ctx* c, int l, T* zf, const T* zc) {
+  Timed tm(c, M_PROLONG);
+  Level& C = c->lev[l + 1];
+  hpg::k_prolong<T><<<grid_for(C.n), 256, 0, c->stream>>>(C.n, C.inj, zf, zc);
+  LAUNCH_CHECK();
+  ++c->launches;
+  return HPG_OK;
+}
+
+template <typename T>
+T* lev_z(Level& L);
+template <>
+double* lev_z<double>(Level& L) { return L.z64; }
+template <>
+float* lev_z<float>(Level& L) { return L.z32; }
+template <typename T>
+T* lev_r(Level& L);
+template <>
+double* lev_r<double>(Level& L) { return L.r64; }
+template <>
+float* lev_r<float>(Level& L) { return L.r32; }
+
+// V-cycle with zero initial guess (ref: multigrid.py:140-171)
+template <typename T>
+int vcycle(hpg_ctx* c, int l, const T* r, T* z) {
+  const bool last = l == c->nlev - 1;
+  const int sweeps = last ? c->nu_c : c->nu1;
+  int rc;
+  for (int s = 0; s < sweeps; ++s)
+    if ((rc = gs_sweep<T>(c, l, r, z, s == 0))) return rc;
+  if (last) return HPG_OK;
+  if ((rc = do_exchange(c, l, sizeof(T) == 8 ? HPG_F64 : HPG_F32, z))) return rc;
+  Level& C = c->lev[l + 1];
+  if ((rc = restrict_<T>(c, l, r, z, lev_r<T>(C)))) return rc;
+  if ((rc = vcycle<T>(c, l + 1, lev_r<T>(C), lev_z<T>(C)))) return rc;
+  if ((rc = prolong_<T>(c, l, z, lev_z<T>(C)))) return rc;
+  for (int s = 0; s < c->nu2; ++s)
+    if ((rc = gs_sweep<T>(c, l, r, z, 0))) return rc;
+  return HPG_OK;
+}
+
+template <typename T, int KB>
+int cgs2_kb(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
+  const int64_t n = c->lev[0].n;
+  T* part = (T*)c->partial;
+  T* scal = (T*)c->scal;
+  const int nb = c->nb;
+  hpg::k_dots<T, KB><<<nb, 256, 0, c->stream>>>(Q, ldq, kb, w, n, part);
+  hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(part, nb, 64, kb, scal, 0);
+  LAUNCH_CHECK();
+  c->launches += 2;
+  int rc;
+  if ((rc = allreduce_scal<T>(c, scal, kb))) return rc;
+  hpg::k_cgs_sub_dots<T, KB><<<nb, 256, 0, c->stream>>>(Q, ldq, kb, w, n, scal, part);
+  hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(part, nb, 64, kb, scal + 64, 0);
+  LAUNCH_CHECK();
+  c->launches += 2;
+  if ((rc = allreduce_scal<T>(c, scal + 64, kb))) return rc;
+  hpg::k_cgs_sub_norm<T, KB><<<nb, 256, 0, c->stream>>>(Q, ldq, kb, w, n, scal + 64, part);
+  LAUNCH_CHECK();
+  c->launches += 1;
+  if (qnext) {
+    hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(part, nb, 64, 1, scal + 128, c->nranks == 1);
+    LAUNCH_CHECK();
+    c->launches += 1;
+    if (c->nranks > 1) {
+      if ((rc = allreduce_scal<T>(c, scal + 128, 1))) return rc;
+      hpg::k_sqrt_inplace<T><<<1, 1, 0, c->stream>>>(scal + 128);
+      c->launches += 1;
+    }
+    hpg::k_scale<T><<<nb, 256, 0, c->stream>>>(w, scal + 128, qnext, n);
+    LAUNCH_CHECK();
+    c->launches += 1;
+  }
+  return HPG_OK;
+}
+
+template <typename T>
+int cgs2_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext, double* out) {
+  const int kb = k + 1;
+  int rc;
+  {
+  Timed tm(c, M_ORTHO);
+  if (kb <= 4) rc = cgs2_kb<T, 4>(c, Q, ldq, kb, w, qnext);
+  else if (kb <= 8) rc = cgs2_kb<T, 8>(c, Q, ldq, kb, w, qnext);
+  else if (kb <= 16) rc = cgs2_kb<T, 16>(c, Q, ldq, kb, w, qnext);
+  else if (kb <= 32) rc = cgs2_kb<T, 32>(c, Q, ldq, kb, w, qnext);
+  else if (kb <= 64) rc = cgs2_kb<T, 64>(c, Q, ldq, kb, w, qnext);
+  else return fail(HPG_E_UNSUPPORTED, "restart basis of %d vectors exceeds 64", kb);
+  if (rc) return rc;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->pinned, c->scal, 129 * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const T* hv = (const T*)c->pinned;
+  for (int j = 0; j < kb; ++j) {
+    out[j] = (double)hv[j];
+    out[kb + j] = (double)hv[64 + j];
+  }
+  out[2 * kb] = qnext ? (double)hv[128] : 0.0;
+  return HPG_OK;
+}
+
+struct YArr {
+  double y[64];
+};
+
+template <typename T, int KB>
+__global__ void k_gemv_combine_y(const T* __restrict__ Q, int64_t ldq, int k, YArr y, T* __restrict__ out,
+                                 int64_t n) {
+  T yr[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) yr[j] = j < k ? (T)y.y[j] : T(0);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    T a = T(0);
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < k) a = fma(Q[j * ldq + i], yr[j], a);
+    out[i] = a;
+  }
+}
+
+template <typename T>
+int gemv_t(hpg_ctx* c, const T* Q, int64_t ldq, int k, const double* y, T* out) {
+  Timed tm(c, M_ORTHO);
+  YArr ya;
+  memset(&ya, 0, sizeof ya);
+  for (int j = 0; j < k; ++j) ya.y[j] = y[j];
+  const int64_t n = c->lev[0].n;
+  if (k <= 8) k_gemv_combine_y<T, 8><<<c->nb, 256, 0, c->stream>>>(Q, ldq, k, ya, out, n);
+  else if (k <= 16) k_gemv_combine_y<T, 16><<<c->nb, 256, 0, c->stream>>>(Q, ldq, k, ya, out, n);
+  else if (k <= 32) k_gemv_combine_y<T, 32><<<c->nb, 256, 0, c->stream>>>(Q, ldq, k, ya, out, n);
+  else if (k <= 64) k_gemv_combine_y<T, 64><<<c->nb, 256, 0, c->stream>>>(Q, ldq, k, ya, out, n);
+  else return fail(HPG_E_UNSUPPORTED, "restart length %d exceeds 64", k);
+  LAUNCH_CHECK();
+  ++c->launches;
+  return HPG_OK;
+}
+
+void free_level(Level& L) {
+  for (void* p : {(void*)L.cols, (void*)L.v64, (void*)L.v32, (void*)L.inj, (void*)L.send_idx, L.send_buf,
+                  (void*)L.z64, (void*)L.z32, (void*)L.r64, (void*)L.r32})
+    if (p) cudaFree(p);
+  L = Level();
+}
+
+template <typename P>
+int dmalloc(P** p, size_t bytes, size_t* acc) {
+  void* q = nullptr;
+  CUDA_TRY(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
+  *p = (P*)q;
+  if (acc) *acc += bytes;
+  return HPG_OK;
+}
+
+int build_level(hpg_ctx* c, Level& L, const int dims[3]) {
+  L.g = make_geom(dims, c->coords, c->procs);
+  L.n = L.g.n;
+  L.n_ext = L.n + L.g.halo_size;
+  L.ld = cdiv(std::max<int64_t>(L.n, 1), 64) * 64;
+  L.nnz = geom_nnz(L.g);
+  if (L.n_ext >= (int64_t)1 << 31) return fail(HPG_E_ARG, "level too large for int32 columns");
+  int rc;
+  const size_t slots = (size_t)27 * L.ld;
+  if ((rc = dmalloc(&L.cols, slots * 4, &L.bytes))) return rc;
+  if ((rc = dmalloc(&L.v64, slots * 8, &L.bytes))) return rc;
+  if ((rc = dmalloc(&L.v32, slots * 4, &L.bytes))) return rc;
+  CUDA_TRY(cudaMemsetAsync(L.cols, 0, slots * 4, c->stream));
+  CUDA_TRY(cudaMemsetAsync(L.v64, 0, slots * 8, c->stream));
+  CUDA_TRY(cudaMemsetAsync(L.v32, 0, slots * 4, c->stream));
+  if (L.n) {
+    hpg::k_build_level<<<grid_for(L.n, 128), 128, 0, c->stream>>>(L.g, L.ld, L.cols, L.v64, L.v32);
+    LAUNCH_CHECK();
+  }
+  // halo plan: one send list per neighbour, in ascending neighbour rank
+  struct Tmp {
+    int rank, idx, sx, sy, sz;
+  };
+  std::vector<Tmp> t;
+  for (int i = 0; i < 27; ++i)
+    if (L.g.nbr_rank[i] >= 0) t.push_back({L.g.nbr_rank[i], i, i % 3 - 1, (i / 3) % 3 - 1, i / 9 - 1});
+  std::sort(t.begin(), t.end(), [](const Tmp& a, const Tmp& b) { return a.rank < b.rank; });
+  int64_t off = 0;
+  for (auto& e : t) {
+    const int64_t cnt = hpg::region_size(L.g, e.sx, e.sy, e.sz);
+    L.nbrs.push_back({e.rank, e.idx, off, cnt, L.g.halo_base[e.idx]});
+    off += cnt;
+  }
+  L.send_total = off;
+  if (off) {
+    if ((rc = dmalloc(&L.send_idx, off * 4, &L.bytes))) return rc;
+    if ((rc = dmalloc((char**)&L.send_buf, off * 8, &L.bytes))) return rc;
+    for (size_t i = 0; i < t.size(); ++i) {
+      const Nbr& nb = L.nbrs[i];
+      hpg::k_build_send<<<grid_for(nb.cnt), 256, 0, c->stream>>>(L.g, t[i].sx, t[i].sy, t[i].sz, nb.cnt,
+                                                                  L.send_idx + nb.send_off);
+      LAUNCH_CHECK();
+    }
+  }
+  if ((rc = dmalloc(&L.z64, L.n_ext * 8, &L.bytes))) return rc;
+  if ((rc = dmalloc(&L.z32, L.n_ext * 4, &L.bytes))) return rc;
+  if ((rc = dmalloc(&L.r64, L.n * 8, &L.bytes))) return rc;
+  if ((rc = dmalloc(&L.r32, L.n * 4, &L.bytes))) return rc;
+  CUDA_TRY(cudaMemsetAsync(L.z64, 0, L.n_ext * 8, c->stream));
+  CUDA_TRY(cudaMemsetAsync(L.z32, 0, L.n_ext * 4, c->stream));
+  return HPG_OK;
+}
+
+int check_prec(int prec) { return prec == HPG_F64 || prec == HPG_F32 ? HPG_OK : fail(HPG_E_ARG, "bad prec %d", prec); }
+int check_level(hpg_ctx* c, int l) {
+  if (!c) return fail(HPG_E_ARG, "null context");
+  return l >= 0 && l < c->nlev ? HPG_OK : fail(HPG_E_ARG, "level %d out of range", l);
+}
+
+}  // namespace
+
+// =============================================================== C ABI
+
+extern "C" {
+
+int hpg_abi_version(void) { return 1; }
+const char* hpg_last_error(void) { return g_err.c_str(); }
+
+int hpg_host_level(const int local_dims[3], const int rank_coords[3], const int proc_dims[3], double* values,
+                   int32_t* col_idx, int32_t* row_nnz, int32_t* diag_pos, int64_t* info, int ninfo) {
+  const Geom g = make_geom(local_dims, rank_coords, proc_dims);
+  for (int64_t i = 0; i < g.n; ++i) {
+    int32_t cols[27];
+    double v[27];
+    int diag = 0;
+    const int nnz = hpg::build_row(g, i, cols, v, &diag);
+    for (int s = 0; s < 27; ++s) {
+      if (values) values[i * 27 + s] = s < nnz ? v[s] : 0.0;
+      if (col_idx) col_idx[i * 27 + s] = s < nnz ? cols[s] : -1;
+    }
+    if (row_nnz) row_nnz[i] = nnz;
+    if (diag_pos) diag_pos[i] = diag;
+  }
+  int64_t tmp[16] = {g.n, g.n + g.halo_size, geom_nnz(g), g.ncolors};
+  for (int k = 0; k < 9; ++k) tmp[4 + k] = g.off[k];
+  tmp[13] = g.halo_size;
+  for (int k = 0; k < ninfo && k < 14; ++k) info[k] = tmp[k];
+  return HPG_OK;
+}
+
+int64_t hpg_host_send_rows(const int local_dims[3], const int rank_coords[3], const int proc_dims[3], int sx, int sy,
+                           int sz, int64_t* rows) {
+  const Geom g = make_geom(local_dims, rank_coords, proc_dims);
+  if (g.halo_base[hpg::offset_index(sx, sy, sz)] < 0) return 0;
+  const int64_t cnt = hpg::region_size(g, sx, sy, sz);
+  if (rows)
+    for (int64_t p = 0; p < cnt; ++p) rows[p] = hpg::send_row(g, sx, sy, sz, p);
+  return cnt;
+}
+
+int hpg_nccl_unique_id(void* out, int len) {
+  if (len < (int)sizeof(ncclUniqueId)) return fail(HPG_E_ARG, "need %zu bytes", sizeof(ncclUniqueId));
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  memcpy(out, &id, sizeof id);
+  return HPG_OK;
+}
+
+int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_dims[3], const int local_dims[3],
+               int levels, int nu1, int nu2, int nu_c, const void* nccl_uid, void* stream) {
+  if (!out) return fail(HPG_E_ARG, "null out");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(HPG_E_ARG, "bad rank %d of %d", rank, nranks);
+  if (proc_dims[0] * proc_dims[1] * proc_dims[2] != nranks) return fail(HPG_E_ARG, "process grid != nranks");
+  if (levels < 1) return fail(HPG_E_ARG, "need at least one level");
+  if (std::min(nu1, std::min(nu2, nu_c)) < 1) return fail(HPG_E_ARG, "sweep counts must all be >= 1");
+  int dims[3] = {local_dims[0], local_dims[1], local_dims[2]};
+  for (int l = 0; l + 1 < levels; ++l)
+    for (int a = 0; a < 3; ++a) {
+      if (dims[a] % 2) return fail(HPG_E_COARSEN, "axis %c: local dimension %d is odd at level %d", "xyz"[a], dims[a], l);
+      dims[a] /= 2;
+    }
+  CUDA_TRY(cudaSetDevice(device));
+  hpg_ctx* c = new hpg_ctx();
+  c->device = device;
+  c->rank = rank;
+  c->nranks = nranks;
+  for (int a = 0; a < 3; ++a) c->procs[a] = proc_dims[a];
+  c->coords[0] = rank % proc_dims[0];
+  c->coords[1] = (rank / proc_dims[0]) % proc_dims[1];
+  c->coords[2] = rank / (proc_dims[0] * proc_dims[1]);
+  c->nlev = levels;
+  c->nu1 = nu1;
+  c->nu2 = nu2;
+  c->nu_c = nu_c;
+  auto bail = [&](int rc) {
+    hpg_destroy(c);
+    return rc;
+  };
+  if (stream) {
+    c->stream = (cudaStream_t)stream;
+    c->own_stream = false;
+  } else if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    return bail(fail(HPG_E_CUDA, "stream create failed"));
+  }
+  c->lev.resize(levels);
+  dims[0] = local_dims[0];
+  dims[1] = local_dims[1];
+  dims[2] = local_dims[2];
+  for (int l = 0; l < levels; ++l) {
+    int rc = build_level(c, c->lev[l], dims);
+    if (rc) return bail(rc);
+    if (l > 0) {
+      Level& C = c->lev[l];
+      rc = dmalloc(&C.inj, std::max<int64_t>(C.n, 1) * 4, &C.bytes);
+      if (rc) return bail(rc);
+      if (C.n) hpg::k_build_inject<<<grid_for(C.n), 256, 0, c->stream>>>(C.g, C.inj);
+    }
+    for (int a = 0; a < 3; ++a) dims[a] /= 2;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  c->nb = (int)std::min<int64_t>(8 * sms, std::max<int64_t>(1, cdiv(c->lev[0].n, 256)));
+  c->spmv_partial_len = grid_for(c->lev[0].n);
+  if (dmalloc((char**)&c->partial, (size_t)c->nb * 64 * 8, nullptr) ||
+      dmalloc(&c->spmv_partial, c->spmv_partial_len * 8, nullptr) ||
+      dmalloc((char**)&c->scal, 256 * 8, nullptr) || dmalloc((char**)&c->gather, (size_t)nranks * 256 * 8, nullptr))
+    return bail(HPG_E_CUDA);
+  if (cudaMallocHost((void**)&c->pinned, 256 * 8) != cudaSuccess) return bail(fail(HPG_E_CUDA, "pinned alloc"));
+  if (nranks > 1) {
+    if (!nccl_uid) return bail(fail(HPG_E_ARG, "nccl_uid required for nranks > 1"));
+    ncclUniqueId id;
+    memcpy(&id, nccl_uid, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess) return bail(fail(HPG_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+  }
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+    return bail(fail(HPG_E_CUDA, "hierarchy build failed"));
+  *out = c;
+  return HPG_OK;
+}
+
+int hpg_destroy(hpg_ctx* c) {
+  if (!c) return HPG_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& L : c->lev) free_level(L);
+  for (void* p : {c->partial, (void*)c->spmv_partial, c->scal, c->gather})
+    if (p) cudaFree(p);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (auto e : c->events) cudaEventDestroy(e);
+  if (c->stream && c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return HPG_OK;
+}
+
+void* hpg_stream(hpg_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int hpg_level_info(hpg_ctx* c, int l, int64_t* info, int ninfo) {
+  int rc = check_level(c, l);
+  if (rc) return rc;
+  const Level& L = c->lev[l];
+  int64_t tmp[20] = {L.n, L.n_ext, L.nnz, L.g.ncolors};
+  for (int k = 0; k < 9; ++k) tmp[4 + k] = L.g.off[k];
+  tmp[13] = L.g.halo_size;
+  tmp[14] = L.ld;
+  tmp[15] = (int64_t)L.nbrs.size();
+  tmp[16] = (int64_t)L.bytes;
+  for (int k = 0; k < ninfo && k < 17; ++k) info[k] = tmp[k];
+  return HPG_OK;
+}
+
+int hpg_export_level(hpg_ctx* c, int l, double* values, int32_t* col_idx, int32_t* row_nnz, int32_t* diag_pos) {
+  int rc = check_level(c, l);
+  if (rc) return rc;
+  const Level& L = c->lev[l];
+  CUDA_TRY(cudaSetDevice(c->device));
+  std::vector<int32_t> cols((size_t)27 * L.ld);
+  std::vector<double> v((size_t)27 * L.ld);
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaMemcpy(cols.data(), L.cols, cols.size() * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(v.data(), L.v64, v.size() * 8, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < L.n; ++i) {
+    int nnz = 0, diag = -1;
+    for (int s = 0; s < 27; ++s) {
+      int32_t cc = cols[s * L.ld + i];
+      const double vv = v[s * L.ld + i];
+      if (cc < 0) {
+        diag = s;
+        cc = ~cc;
+      }
+      if (vv != 0.0) nnz = s + 1;
+      if (values) values[i * 27 + s] = vv;
+      if (col_idx) col_idx[i * 27 + s] = cc;
+    }
+    for (int s = nnz; s < 27; ++s)
+      if (col_idx) col_idx[i * 27 + s] = -1;
+    if (row_nnz) row_nnz[i] = nnz;
+    if (diag_pos) diag_pos[i] = diag;
+  }
+  return HPG_OK;
+}
+
+int hpg_export_f2c(hpg_ctx* c, int l, int64_t* f2c) {
+  int rc = check_level(c, l);
+  if (rc) return rc;
+  if (l == 0) return fail(HPG_E_ARG, "level 0 has no injection map");
+  const Level& C = c->lev[l];
+  std::vector<int32_t> dst(C.n);
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaMemcpy(dst.data(), C.inj, C.n * 4, cudaMemcpyDeviceToHost));
+  for (int64_t j = 0; j < C.n; ++j) f2c[dst[j]] = j;  // fine color-0 row j feeds coarse row dst[j]
+  return HPG_OK;
+}
+
+int hpg_spmv(hpg_ctx* c, int l, int prec, void* x, void* y) {
+  int rc = check_level(c, l);
+  if (rc || (rc = check_prec(prec))) return rc;
+  Timed tm(c, M_SPMV);
+  if ((rc = do_exchange(c, l, prec, x))) return rc;
+  Level& L = c->lev[l];
+  if (!L.n) return HPG_OK;
+  if (prec == HPG_F64)
+    hpg::k_spmv<double, 0><<<grid_for(L.n), 256, 0, c->stream>>>(L.cols, L.v64, L.ld, 0, L.n, (const double*)x,
+                                                                  nullptr, (double*)y, nullptr);
+  else
+    hpg::k_spmv<float, 0><<<grid_for(L.n), 256, 0, c->stream>>>(L.cols, L.v32, L.ld, 0, L.n, (const float*)x,
+                                                                 nullptr, (float*)y, nullptr);
+  LAUNCH_CHECK();
+  ++c->launches;
+  return HPG_OK;
+}
+
+int hpg_exchange(hpg_ctx* c, int l, int prec, void* v) {
+  int rc = check_level(c, l);
+  if (rc || (rc = check_prec(prec))) return rc;
+  return do_exchange(c, l, prec, v);
+}
+
+int hpg_gs_sweep(hpg_ctx* c, int l, int prec, const void* r, void* z, int z_is_zero) {
+  int rc = check_level(c, l);
+  if (rc || (rc = check_prec(prec))) return rc;
+  return prec == HPG_F64 ? gs_sweep<double>(c, l, (const double*)r, (double*)z, z_is_zero)
+                         : gs_sweep<float>(c, l, (const float*)r, (float*)z, z_is_zero);
+}
+
+int hpg_restrict(hpg_ctx* c, int l, int prec, const void* rf, const void* zf, void* rcoarse) {
+  int rc = check_level(c, l);
+  if (rc || (rc = check_prec(prec))) return rc;
+  if (l + 1 >= c->nlev) return fail(HPG_E_ARG, "level %d has no coarser level", l);
+  return prec == HPG_F64 ? restrict_<double>(c, l, (const double*)rf, (const double*)zf, (double*)rcoarse)
+                         : restrict_<float>(c, l, (const float*)rf, (const float*)zf, (float*)rcoarse);
+}
+
+int hpg_prolong(hpg_ctx* c, int l, int prec, void* zf, const void* zc) {
+  int rc = check_level(c, l);
+  if (rc || (rc = check_prec(prec))) return rc;
+  if (l + 1 >= c->nlev) return fail(HPG_E_ARG, "level %d has no coarser level", l);
+  return prec == HPG_F64 ? prolong_<double>(c, l, (double*)zf, (const double*)zc)
+                         : prolong_<float>(c, l, (float*)zf, (const float*)zc);
+}
+
+int hpg_vcycle(hpg_ctx* c, int prec, const void* r, void* z) {
+  int rc = check_level(c, 0);
+  if (rc || (rc = check_prec(prec))) return rc;
+  return prec == HPG_F64 ? vcycle<double>(c, 0, (const double*)r, (double*)z)
+                         : vcycle<float>(c, 0, (const float*)r, (float*)z);
+}
+
+int hpg_cgs2(hpg_ctx* c, int prec, void* Q, int64_t ldq, int k, void* w, void* qnext, double* out) {
+  int rc = check_level(c, 0);
+  if (rc || (rc = check_prec(prec))) return rc;
+  if (k < 0) return fail(HPG_E_ARG, "bad k");
+  return prec == HPG_F64 ? cgs2_t<double>(c, (double*)Q, ldq, k, (double*)w, (double*)qnext, out)
+                         : cgs2_t<float>(c, (float*)Q, ldq, k, (float*)w, (float*)qnext, out);
+}
+
+int hpg_gemv_combine(hpg_ctx* c, int prec, const void* Q, int64_t ldq, int k, const double* y, void* out) {
+  int rc = check_level(c, 0);
+  if (rc || (rc = check_prec(prec))) return rc;
+  if (k < 1) return fail(HPG_E_ARG, "bad k");
+  return prec == HPG_F64 ? gemv_t<double>(c, (const double*)Q, ldq, k, y, (double*)out)
+                         : gemv_t<float>(c, (const float*)Q, ldq, k, y, (float*)out);
+}
+
+int hpg_axpy_mixed(hpg_ctx* c, int prec, double* x, const void* z, int64_t n) {
+  int rc = check_level(c, 0);
+  if (rc || (rc = check_prec(prec))) return rc;
+  Timed tm(c, M_VEC);
+  if (prec == HPG_F64)
+    hpg::k_axpy_mixed<double><<<c->nb, 256, 0, c->stream>>>(x, (const double*)z, n);
+  else
+    hpg::k_axpy_mixed<float><<<c->nb, 256, 0, c->stream>>>(x, (const float*)z, n);
+  LAUNCH_CHECK();
+  ++c->launches;
+  return HPG_OK;
+}
+
+int hpg_residual(hpg_ctx* c, const double* b, double* x, double* r, double* rho2) {
+  int rc = check_level(c, 0);
+  if (rc) return rc;
+  {
+  Timed tm(c, M_SPMV);
+  if ((rc = do_exchange(c, 0, HPG_F64, x))) return rc;
+  Level& L = c->lev[0];
+  double* scal = (double*)c->scal;
+  const int nbk = grid_for(L.n);
+  hpg::k_spmv<double, 1><<<nbk, 256, 0, c->stream>>>(L.cols, L.v64, L.ld, 0, L.n, x, b, r, c->spmv_partial);
+  hpg::k_fold<double><<<1, 1024, 0, c->stream>>>(c->spmv_partial, nbk, 1, 1, scal + 200, 0);
+  LAUNCH_CHECK();
+  c->launches += 2;
+  if ((rc = allreduce_scal<double>(c, scal + 200, 1))) return rc;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->pinned + 200, (double*)c->scal + 200, 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  *rho2 = c->pinned[200];
+  return HPG_OK;
+}
+
+int hpg_scale_cast(hpg_ctx* c, int prec, const double* r, double rho, void* q0, int64_t n) {
+  int rc = check_level(c, 0);
+  if (rc || (rc = check_prec(prec))) return rc;
+  Timed tm(c, M_VEC);
+  if (prec == HPG_F64)
+    hpg::k_scale_cast<double><<<c->nb, 256, 0, c->stream>>>(r, rho, (double*)q0, n);
+  else
+    hpg::k_scale_cast<float><<<c->nb, 256, 0, c->stream>>>(r, rho, (float*)q0, n);
+  LAUNCH_CHECK();
+  ++c->launches;
+  return HPG_OK;
+}
+
+int hpg_sumsq(hpg_ctx* c, int prec, const void* x, int64_t n, double* out) {
+  int rc = check_level(c, 0);
+  if (rc || (rc = check_prec(prec))) return rc;
+  const int nb = (int)std::min<int64_t>(c->nb, std::max<int64_t>(1, cdiv(n, 256)));
+  Timed tm(c, M_VEC);
+  if (prec == HPG_F64) {
+    double* scal = (double*)c->scal;
+    hpg::k_sumsq<double><<<nb, 256, 0, c->stream>>>((const double*)x, n, (double*)c->partial);
+    hpg::k_fold<double><<<1, 1024, 0, c->stream>>>((const double*)c->partial, nb, 64, 1, scal + 210, 0);
+    LAUNCH_CHECK();
+    if ((rc = allreduce_scal<double>(c, scal + 210, 1))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->pinned + 210, scal + 210, 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *out = c->pinned[210];
+  } else {
+    float* scal = (float*)c->scal;
+    hpg::k_sumsq<float><<<nb, 256, 0, c->stream>>>((const float*)x, n, (float*)c->partial);
+    hpg::k_fold<float><<<1, 1024, 0, c->stream>>>((const float*)c->partial, nb, 64, 1, scal + 420, 0);
+    LAUNCH_CHECK();
+    if ((rc = allreduce_scal<float>(c, scal + 420, 1))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->pinned + 210, scal + 420, 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *out = (double)*(float*)(c->pinned + 210);
+  }
+  c->launches += 2;
+  return HPG_OK;
+}
+
+int hpg_sync(hpg_ctx* c) {
+  if (!c) return fail(HPG_E_ARG, "null context");
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return HPG_OK;
+}
+
+int hpg_allreduce_host(hpg_ctx* c, double* vals, int n) {
+  if (!c) return fail(HPG_E_ARG, "null context");
+  if (c->nranks == 1) return HPG_OK;
+  if (n > 32) return fail(HPG_E_ARG, "at most 32 values");
+  double* scal = (double*)c->scal;
+  CUDA_TRY(cudaMemcpyAsync(scal + 220, vals, n * 8, cudaMemcpyHostToDevice, c->stream));
+  int rc = allreduce_scal<double>(c, scal + 220, n);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(vals, scal + 220, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return HPG_OK;
+}
+
+int64_t hpg_launch_count(hpg_ctx* c) { return c ? c->launches : -1; }
+
+// mode 1: enable, 0: disable, 2: synchronise, add each motif's seconds into
+// seconds[6] (GS, SpMV, Ortho, Restriction, Prolongation, Vector ops) and reset.
+int hpg_timers(hpg_ctx* c, int mode, double* seconds) {
+  if (!c) return fail(HPG_E_ARG, "null context");
+  if (mode == 0 || mode == 1) {
+    c->timing = mode == 1;
+    return HPG_OK;
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  for (auto& m : c->marks) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->events[m.second], c->events[m.second + 1]));
+    if (seconds) seconds[m.first] += ms * 1e-3;
+  }
+  c->marks.clear();
+  c->ev_used = 0;
+  return HPG_OK;
+}
+
+}  // extern "C"

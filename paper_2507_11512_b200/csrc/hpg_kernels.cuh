@@ -1,0 +1,363 @@
+// sm_100a kernels of the HPG-MxP solve path.
+//
+// Layout (per level):
+//   cols  int32 [27][ld]  slot-major ELL ("column-major"), ld = n rounded up to 64
+//   v64   f64   [27][ld]  values, compacted rows, ascending global column
+//   v32   f32   [27][ld]  the same values narrowed (26 / -1 / 0 are exact)
+// The diagonal slot stores ~col (negative) instead of col, so the smoother
+// finds a_ii without a separate diag_pos stream; padding slots hold column 0
+// and value 0 exactly like the reference's spmv_cols (ref: problem.py:59-65).
+//
+// Stencil kernels reproduce the reference's arithmetic bitwise: per row the
+// 27 products are accumulated in slot order with separate IEEE multiply and
+// add (no FMA contraction), closed by an IEEE subtract / divide
+// (ref: krylov.py:76-80, smoother.py:62-75, multigrid.py:107-128).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hpg {
+
+// ---------------------------------------------------------------- arithmetic
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+
+// streaming loads for the matrix planes: read once, do not pollute L1,
+// evict first from L2 so the gathered vectors stay resident
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// ------------------------------------------------------------ stencil kernels
+
+// y[i] = sum_s A[i,s] x[col[i,s]]  for rows [row0, row0+nrows)
+// MODE 0: y = Ax.  MODE 1: y = b - Ax and per-block partial of sum y^2 (fp64 outer residual).
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) k_spmv(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+                                              int64_t ld, int64_t row0, int64_t nrows,
+                                              const T* __restrict__ x, const T* __restrict__ b,
+                                              T* __restrict__ y, double* __restrict__ partial) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double sq = 0.0;
+  if (t < nrows) {
+    const int64_t i = row0 + t;
+    T acc = T(0);
+#pragma unroll
+    for (int s = 0; s < 27; ++s) {
+      int32_t c = ld_stream(cols + s * ld + i);
+      const T v = ld_stream(vals + s * ld + i);
+      c = c < 0 ? ~c : c;
+      acc = add_rn(acc, mul_rn(v, x[c]));
+    }
+    if (MODE == 0) {
+      y[i] = acc;
+    } else {
+      const T r = sub_rn(b[i], acc);
+      y[i] = r;
+      sq = (double)r * (double)r;
+    }
+  }
+  if (MODE == 1) {
+    // deterministic block reduction of the squared residual
+    __shared__ double red[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += red[w];
+      partial[blockIdx.x] = a;
+    }
+  }
+}
+
+// One color pass of forward Gauss-Seidel over rows [row0, row0+nrows):
+//   z_i = (r_i - sum_{s != diag} A[i,s] z[col]) / a_ii
+// The diagonal slot contributes 0 * z_i exactly like the reference's zeroed
+// offvals (ref: smoother.py:44-46, 62-66).
+template <typename T>
+__global__ void __launch_bounds__(256) k_gs_pass(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+                                                 int64_t ld, int64_t row0, int64_t nrows,
+                                                 const T* __restrict__ r, T* z) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrows) return;
+  const int64_t i = row0 + t;
+  T acc = T(0);
+  T d = T(0);
+#pragma unroll
+  for (int s = 0; s < 27; ++s) {
+    int32_t c = ld_stream(cols + s * ld + i);
+    T v = ld_stream(vals + s * ld + i);
+    if (c < 0) {
+      d = v;
+      v = T(0);
+      c = ~c;
+    }
+    acc = add_rn(acc, mul_rn(v, z[c]));
+  }
+  z[i] = div_rn(sub_rn(r[i], acc), d);
+}
+
+// Fused residual + injection: for fine color-0 row j < nc,
+//   rc[dst[j]] = r[j] - (A z)[j]     (ref: multigrid.py:107-128)
+template <typename T>
+__global__ void __launch_bounds__(256) k_restrict(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+                                                  int64_t ld, int64_t nc, const int32_t* __restrict__ dst,
+                                                  const T* __restrict__ r, const T* __restrict__ z,
+                                                  T* __restrict__ rc) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nc) return;
+  T acc = T(0);
+#pragma unroll
+  for (int s = 0; s < 27; ++s) {
+    int32_t c = ld_stream(cols + s * ld + j);
+    const T v = ld_stream(vals + s * ld + j);
+    c = c < 0 ? ~c : c;
+    acc = add_rn(acc, mul_rn(v, z[c]));
+  }
+  rc[dst[j]] = sub_rn(r[j], acc);
+}
+
+// Injection transpose: z[j] += zc[dst[j]]  (ref: multigrid.py:131-137)
+template <typename T>
+__global__ void k_prolong(int64_t nc, const int32_t* __restrict__ dst, T* __restrict__ z,
+                          const T* __restrict__ zc) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nc) return;
+  z[j] = add_rn(z[j], zc[dst[j]]);
+}
+
+// ---------------------------------------------------------- halo pack
+
+template <typename T>
+__global__ void k_pack(const T* __restrict__ v, const int32_t* __restrict__ idx, int64_t cnt,
+                       T* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < cnt) out[e] = v[idx[e]];
+}
+
+// --------------------------------------------------------- Krylov vectors
+// Deterministic two-stage reductions: every kernel writes one partial per
+// block (fixed grid), a single-block fold sums them in a fixed tree order.
+
+template <int KB, typename T>
+__device__ __forceinline__ void block_reduce_store(T (&acc)[KB], int kb, T* out) {
+  __shared__ T red[8][KB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+    T a = acc[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) red[warp][j] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x < kb) {
+    T a = red[0][threadIdx.x];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) a += red[w][threadIdx.x];
+    out[threadIdx.x] = a;
+  }
+}
+
+// partial[b][j] = sum_{i in block b} Q[j][i] * w[i],  j < kb
+template <typename T, int KB>
+__global__ void __launch_bounds__(256) k_dots(const T* __restrict__ Q, int64_t ldq, int kb,
+                                              const T* __restrict__ w, int64_t n, T* __restrict__ partial) {
+  T acc[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) acc[j] = T(0);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const T wi = w[i];
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < kb) acc[j] = fma(Q[j * ldq + i], wi, acc[j]);
+  }
+  block_reduce_store<KB>(acc, kb, partial + (int64_t)blockIdx.x * 64);
+}
+
+// CGS pass-1 correction fused with the pass-2 projection:
+//   w_i -= sum_j Q[j][i] h[j];  partial[b][j] = sum Q[j][i] w_i(new)
+template <typename T, int KB>
+__global__ void __launch_bounds__(256) k_cgs_sub_dots(const T* __restrict__ Q, int64_t ldq, int kb,
+                                                      T* __restrict__ w, int64_t n, const T* __restrict__ h,
+                                                      T* __restrict__ partial) {
+  T acc[KB], hr[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+    acc[j] = T(0);
+    hr[j] = j < kb ? h[j] : T(0);
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    T q[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) q[j] = j < kb ? Q[j * ldq + i] : T(0);
+    T tsum = T(0);
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < kb) tsum = fma(q[j], hr[j], tsum);
+    const T wi = w[i] - tsum;
+    w[i] = wi;
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < kb) acc[j] = fma(q[j], wi, acc[j]);
+  }
+  block_reduce_store<KB>(acc, kb, partial + (int64_t)blockIdx.x * 64);
+}
+
+// CGS pass-2 correction fused with the norm: w_i -= sum_j Q[j][i] h[j]; partial[b] = sum w_i^2
+template <typename T, int KB>
+__global__ void __launch_bounds__(256) k_cgs_sub_norm(const T* __restrict__ Q, int64_t ldq, int kb,
+                                                      T* __restrict__ w, int64_t n, const T* __restrict__ h,
+                                                      T* __restrict__ partial) {
+  T hr[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) hr[j] = j < kb ? h[j] : T(0);
+  T acc[1] = {T(0)};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    T tsum = T(0);
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < kb) tsum = fma(Q[j * ldq + i], hr[j], tsum);
+    const T wi = w[i] - tsum;
+    w[i] = wi;
+    acc[0] = fma(wi, wi, acc[0]);
+  }
+  block_reduce_store<1>(acc, 1, partial + (int64_t)blockIdx.x * 64);
+}
+
+// Single-block fold of nb partial rows (row stride `stride`) into out[j], j < kb.
+// One warp per output, lanes stride over the blocks, fixed shuffle tree:
+// the same bits on every run.
+template <typename T>
+__global__ void k_fold(const T* __restrict__ partial, int nb, int stride, int kb, T* __restrict__ out,
+                       int do_sqrt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < kb; j += nw) {
+    T a = T(0);
+    for (int b = lane; b < nb; b += 32) a += partial[(int64_t)b * stride + j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) out[j] = do_sqrt ? sqrt(a) : a;
+  }
+}
+
+// fold over ranks in ascending rank order (ref: comm.py:97-108): out[j] = sum_r g[r*cnt+j]
+template <typename T>
+__global__ void k_fold_ranks(const T* __restrict__ g, int nranks, int cnt, T* __restrict__ out, int sqrt_first) {
+  const int j = threadIdx.x;
+  if (j >= cnt) return;
+  T a = g[j];
+  for (int r = 1; r < nranks; ++r) a = a + g[(int64_t)r * cnt + j];
+  out[j] = (sqrt_first && j == 0) ? sqrt(a) : a;
+}
+
+template <typename T>
+__global__ void k_sqrt_inplace(T* v) {
+  v[0] = sqrt(v[0]);
+}
+
+// Q[k+1] = w / beta  (0 when beta == 0)  (ref: krylov.py:267-273)
+template <typename T>
+__global__ void k_scale(const T* __restrict__ w, const T* __restrict__ beta, T* __restrict__ q, int64_t n) {
+  const T bt = *beta;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    q[i] = bt != T(0) ? div_rn(w[i], bt) : T(0);
+}
+
+// Q0 = (T)(r / rho) computed in fp64 then narrowed (ref: krylov.py:250-252)
+template <typename T>
+__global__ void k_scale_cast(const double* __restrict__ r, double rho, T* __restrict__ q, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    q[i] = (T)__ddiv_rn(r[i], rho);
+}
+
+// out[i] = sum_{j<k} Q[j][i] y[j]   (ref: krylov.py:288-289)
+template <typename T, int KB>
+__global__ void __launch_bounds__(256) k_gemv_combine(const T* __restrict__ Q, int64_t ldq, int k,
+                                                      const T* __restrict__ y, T* __restrict__ out, int64_t n) {
+  T yr[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) yr[j] = j < k ? y[j] : T(0);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    T a = T(0);
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < k) a = fma(Q[j * ldq + i], yr[j], a);
+    out[i] = a;
+  }
+}
+
+// x += z (fp64 += promoted z)   (ref: krylov.py:292-293)
+template <typename T>
+__global__ void k_axpy_mixed(double* __restrict__ x, const T* __restrict__ z, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = __dadd_rn(x[i], (double)z[i]);
+}
+
+// partial sum of x^2 (norms of b and of arbitrary vectors)
+template <typename T>
+__global__ void __launch_bounds__(256) k_sumsq(const T* __restrict__ x, int64_t n, T* __restrict__ partial) {
+  T acc[1] = {T(0)};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc[0] = fma(x[i], x[i], acc[0]);
+  block_reduce_store<1>(acc, 1, partial + (int64_t)blockIdx.x * 64);
+}
+
+// -------------------------------------------------------------- setup
+
+__global__ void k_build_level(Geom g, int64_t ld, int32_t* __restrict__ cols, double* __restrict__ v64,
+                              float* __restrict__ v32) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  int32_t c[27];
+  double v[27];
+  int diag = 0;
+  const int nnz = build_row(g, i, c, v, &diag);
+  for (int s = 0; s < 27; ++s) {
+    int32_t cc = 0;
+    double vv = 0.0;
+    if (s < nnz) {
+      cc = s == diag ? ~c[s] : c[s];
+      vv = v[s];
+    }
+    cols[s * ld + i] = cc;
+    v64[s * ld + i] = vv;
+    v32[s * ld + i] = (float)vv;
+  }
+}
+
+// dst[j] = coarse iperm of coarse natural index j   (f2c inverse on color-0 rows)
+__global__ void k_build_inject(Geom gc, int32_t* __restrict__ dst) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= gc.n) return;
+  const int x = (int)(j % gc.lx);
+  const int y = (int)((j / gc.lx) % gc.ly);
+  const int z = (int)(j / ((int64_t)gc.lx * gc.ly));
+  dst[j] = (int32_t)iperm(gc, x, y, z);
+}
+
+__global__ void k_build_send(Geom g, int sx, int sy, int sz, int64_t cnt, int32_t* __restrict__ idx) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < cnt) idx[p] = (int32_t)send_row(g, sx, sy, sz, p);
+}
+
+}  // namespace hpg

@@ -1,0 +1,203 @@
+"""Geometric multigrid on the device (ref: multigrid.py:1-172).
+
+``build_hierarchy`` creates one libhpgmxp context that generates every level
+in HBM (csrc/hpg_capi.cu build_level): permuted ELL in fp64 and fp32,
+halo plans, injection maps and V-cycle workspaces.  ``MgHierarchy.apply``
+runs the whole V-cycle inside the library (one C call, no host round trips);
+``mg_vcycle`` is the same algorithm spelled out over the per-kernel entry
+points, kept for API parity and as a differential test of ``apply``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .coloring import color as color_rows
+from .comm import HaloPlan
+from .device import Context
+from .problem import EllMatrix
+from .smoother import SmootherWorkspace, forward_gs_sweep
+
+
+@dataclass
+class MgLevel:
+    domain: object
+    A_hi: object
+    A_lo: object
+    coloring: object = None
+    plan: object = None
+    f2c: object = None
+    z_hi: object = None
+    z_lo: object = None
+    r_hi: object = None
+    r_lo: object = None
+
+
+@dataclass
+class MgHierarchy:
+    levels: list
+    sweeps: SmootherWorkspace
+    world: object = None
+    rank: int = 0
+    ctx: object = field(default=None, repr=False)
+
+    def apply(self, r, tally=None, out=None):
+        """One V-cycle from the finest level; precision follows r's dtype (ref: multigrid.py:49-51).
+
+        Returns the level-0 workspace view (or ``out[:n]`` when given, out having
+        the halo tail) -- consume it before the next call, like the reference.
+        """
+        import torch
+        lv = self.levels[0]
+        lo = r.dtype == torch.float32
+        A = lv.A_lo if lo else lv.A_hi
+        z = out if out is not None else (lv.z_lo if lo else lv.z_hi)
+        self.ctx.call("hpg_vcycle", A.prec, _lib.ptr(r), _lib.ptr(z))
+        if tally is not None:
+            count_vcycle(self, tally, A.dtype)
+        return z[:A.n_rows]
+
+    def preconditioner(self, tally=None):
+        """Callable precond(r, out=None) for gmres_solve (writes into out when given)."""
+        hier = self
+
+        def precond(r, out=None):
+            return hier.apply(r, tally, out)
+
+        precond.accepts_out = True
+        return precond
+
+    def close(self):
+        if self.ctx is not None:
+            self.ctx.close()
+            self.ctx = None
+
+
+def count_vcycle(h, tally, dtype):
+    """Flop/byte accounting of one V-cycle, call by call as the reference tallies it."""
+    nl = len(h.levels)
+    sw = h.sweeps
+    for lev in range(nl):
+        A = h.levels[lev].A_hi
+        last = lev == nl - 1
+        sweeps = sw.nu_c if last else sw.nu1 + sw.nu2
+        for _ in range(sweeps):
+            tally.add("gs_sweep", dtype, nnz=A.nnz_total, n=A.n_rows)
+        if not last:
+            nxt = h.levels[lev + 1]
+            tally.add("restrict_fused", dtype, nnz=nxt.inject_nnz, n_c=nxt.A_hi.n_rows)
+            tally.add("prolong_add", dtype, n_c=nxt.A_hi.n_rows)
+
+
+def _inject_nnz(domain):
+    """nnz of the fine rows at injection points (even local coords) -- closed form."""
+    tot = 1
+    for l, o, g in ((domain.lnx, domain.ox, domain.gnx), (domain.lny, domain.oy, domain.gny),
+                    (domain.lnz, domain.oz, domain.gnz)):
+        s = 0
+        for x in range(0, l, 2):
+            s += sum(1 for d in (-1, 0, 1) if 0 <= o + x + d < g)
+        tot *= s
+    return tot
+
+
+def build_hierarchy(domain, levels, world=None, rank=0, strategy="greedy", seed=0, sweeps=None):
+    """Generate, color, reorder and plan every level on the device (ref: multigrid.py:54-84)."""
+    import torch
+    if levels < 1:
+        raise ValueError("need at least one level")
+    if strategy != "greedy":
+        color_rows(domain, strategy)  # raises NotImplementedError with the reason
+    sweeps = sweeps or SmootherWorkspace()
+    doms = [domain]
+    for _ in range(levels - 1):
+        doms.append(doms[-1].coarsen())  # CoarseningError, like the reference
+    ctx = Context(domain, levels, sweeps.nu1, sweeps.nu2, sweeps.nu_c, world)
+    out = []
+    for lev, dom in enumerate(doms):
+        A = EllMatrix(ctx, lev, _lib.F64)
+        A_lo = EllMatrix(ctx, lev, _lib.F32)
+        A.domain = A_lo.domain = dom
+        lv = MgLevel(domain=dom, A_hi=A, A_lo=A_lo)
+        lv.plan = HaloPlan(ctx, lev, dom) if world is not None else None
+        ne, n = A.n_cols_extended, A.n_rows
+        dev = ctx.device
+        lv.z_hi = torch.zeros(ne, dtype=torch.float64, device=dev)
+        lv.z_lo = torch.zeros(ne, dtype=torch.float32, device=dev)
+        lv.r_hi = torch.zeros(n, dtype=torch.float64, device=dev)
+        lv.r_lo = torch.zeros(n, dtype=torch.float32, device=dev)
+        if lev > 0:
+            lv.inject_nnz = _inject_nnz(doms[lev - 1])
+        out.append(lv)
+    return MgHierarchy(levels=out, sweeps=sweeps, world=world, rank=rank, ctx=ctx)
+
+
+def level_coloring(lv):
+    if lv.coloring is None:
+        lv.coloring = color_rows(lv.domain)
+    return lv.coloring
+
+
+def injection_map(h, level):
+    """f2c of ``level`` (>= 1) into its parent, as host int64 (ref: multigrid.py:87-99)."""
+    import ctypes as C
+    n = h.levels[level].A_hi.n_rows
+    f2c = np.zeros(n, dtype=np.int64)
+    h.ctx.call("hpg_export_f2c", level, f2c.ctypes.data_as(C.POINTER(C.c_int64)))
+    return f2c
+
+
+def restrict_inject(v_f, f2c):
+    """Coarse vector of the fine values at injection points (ref: multigrid.py:102-104)."""
+    return v_f[f2c].clone()
+
+
+def fused_residual_restrict(A_f, b_f, x_f, f2c=None, out=None, tally=None, n_c=None):
+    """r_c = (b_f - A_f x_f) at the injected rows; x_f's halo must be fresh (ref: multigrid.py:107-128).
+
+    ``A_f`` is the fine level's operand; the injection map is the coarse level's
+    (built on the device), so ``f2c`` is accepted for signature parity only.
+    """
+    import torch
+    info = A_f.ctx.level_info(A_f.level + 1)
+    if out is None:
+        out = torch.empty(info["n"], dtype=A_f.torch_dtype, device=x_f.device)
+    A_f.ctx.call("hpg_restrict", A_f.level, A_f.prec, _lib.ptr(b_f), _lib.ptr(x_f), _lib.ptr(out))
+    if tally is not None:
+        tally.add("restrict_fused", A_f.dtype, nnz=_inject_nnz(A_f.domain), n_c=info["n"])
+    return out
+
+
+def prolong_add(A_f, x_f, x_c, tally=None):
+    """x_f[f2c] += x_c on the device (ref: multigrid.py:131-137); A_f names the fine level."""
+    A_f.ctx.call("hpg_prolong", A_f.level, A_f.prec, _lib.ptr(x_f), _lib.ptr(x_c))
+    if tally is not None:
+        tally.add("prolong_add", A_f.dtype, n_c=x_c.numel())
+
+
+def mg_vcycle(h, level, r, tally=None):
+    """The V-cycle over the per-kernel entry points (ref: multigrid.py:140-171)."""
+    import torch
+    lv = h.levels[level]
+    lo = r.dtype == torch.float32
+    A = lv.A_lo if lo else lv.A_hi
+    z = lv.z_lo if lo else lv.z_hi
+    sw = h.sweeps
+    last = level == len(h.levels) - 1
+    for s in range(sw.nu_c if last else sw.nu1):
+        forward_gs_sweep(A, r, z, z_is_zero=(s == 0), tally=tally)
+    if last:
+        return z[:A.n_rows]
+    if h.world is not None:
+        lv.plan.exchange(z)
+    nxt = h.levels[level + 1]
+    rc = nxt.r_lo if lo else nxt.r_hi
+    fused_residual_restrict(A, r, z, out=rc, tally=tally)
+    zc = mg_vcycle(h, level + 1, rc, tally)
+    prolong_add(A, z, zc, tally=tally)
+    for _ in range(sw.nu2):
+        forward_gs_sweep(A, r, z, tally=tally)
+    return z[:A.n_rows]
