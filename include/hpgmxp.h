@@ -131,6 +131,10 @@ int64_t hpg_launch_count(hpg_ctx* ctx);
  * 0 disable, 2 synchronise + ADD seconds per motif into seconds[6]
  * (GS, SpMV, Ortho, Restriction, Prolongation, Vector ops) and reset.      */
 int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
+/* Tuning switches (results are identical up to reduction order):
+ *   "cgs_fused"  1: single-rank CGS2 as one cooperative bulk-copy kernel, 0: per-pass kernels
+ *   "tail_rows"  levels with at most this many rows run in the persistent V-cycle tail kernel */
+int hpg_set_option(hpg_ctx* ctx, const char* key, int64_t value);
 
 #ifdef __cplusplus
 }

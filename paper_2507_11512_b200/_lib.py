@@ -55,6 +55,7 @@ SIGNATURES = {
     "hpg_allreduce_host": (_i, [_p, _dp, _i]),
     "hpg_launch_count": (_i64, [_p]),
     "hpg_timers": (_i, [_p, _i, _dp]),
+    "hpg_set_option": (_i, [_p, C.c_char_p, _i64]),
 }
 
 _LIB = None

@@ -1,11 +1,14 @@
 // libhpgmxp.so: context, hierarchy build, and the extern "C" entry points
 // declared in include/hpgmxp.h.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -13,6 +16,8 @@
 #include "hpgmxp.h"
 #include "hpg_geom.h"
 #include "hpg_kernels.cuh"
+#include "hpg_coarse.cuh"
+#include "hpg_cgs.cuh"
 
 using hpg::Geom;
 
@@ -52,6 +57,15 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Row stride of slot-major planes: a multiple of 32 elements that is an ODD
+// multiple of 128 B, so the 27 concurrent plane streams of a warp do not
+// alias onto the same L2 slices (2^k strides would).
+inline int64_t pad_ld(int64_t n) {
+  int64_t ld = cdiv(std::max<int64_t>(n, 1), 32) * 32;
+  if ((ld / 32) % 2 == 0) ld += 32;
+  return ld;
+}
 
 // ------------------------------------------------------------------ geometry (host)
 
@@ -166,6 +180,9 @@ struct hpg_ctx {
   void* gather = nullptr;       // nranks * 256
   double* pinned = nullptr;     // 256 host doubles
   int64_t launches = 0;
+  bool cgs_fused = true;
+  int64_t tail_rows = 0;        // levels with n <= tail_rows run in the persistent tail kernel
+  int tail_blocks[2] = {0, 0};  // cooperative grid (f64, f32)
   // per-motif CUDA-event timers (ref: metrics.py:125-131 Tally.timed)
   bool timing = false;
   std::vector<cudaEvent_t> events;
@@ -298,9 +315,42 @@ double* lev_r<double>(Level& L) { return L.r64; }
 template <>
 float* lev_r<float>(Level& L) { return L.r32; }
 
+template <typename T>
+int vcycle_tail(hpg_ctx* c, int l, const T* r, T* z) {
+  Timed tm(c, M_GS);
+  hpg::TailParams<T> p;
+  memset(&p, 0, sizeof p);
+  p.nl = c->nlev - l;
+  p.nu1 = c->nu1;
+  p.nu2 = c->nu2;
+  p.nu_c = c->nu_c;
+  for (int k = 0; k < p.nl; ++k) {
+    Level& L = c->lev[l + k];
+    hpg::TailLevel<T>& t = p.lv[k];
+    t.cols = L.cols;
+    t.vals = vals_of<T>(L);
+    t.inj = L.inj;
+    t.z = k == 0 ? z : lev_z<T>(L);
+    t.r = k == 0 ? (T*)r : lev_r<T>(L);
+    t.ld = L.ld;
+    t.n = L.n;
+    t.n_ext = L.n_ext;
+    for (int q = 0; q < 9; ++q) t.off[q] = L.g.off[q];
+    t.ncolors = L.g.ncolors;
+  }
+  const int blocks = c->tail_blocks[sizeof(T) == 4];
+  void* args[] = {(void*)&p};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)hpg::k_vcycle_tail<T>, dim3(blocks), dim3(256), args, 0,
+                                       c->stream));
+  ++c->launches;
+  return HPG_OK;
+}
+
 // V-cycle with zero initial guess (ref: multigrid.py:140-171)
 template <typename T>
 int vcycle(hpg_ctx* c, int l, const T* r, T* z) {
+  if (c->nranks == 1 && l > 0 && c->lev[l].n <= c->tail_rows && c->nlev - l <= hpg::kMaxTail)
+    return vcycle_tail<T>(c, l, r, z);
   const bool last = l == c->nlev - 1;
   const int sweeps = last ? c->nu_c : c->nu1;
   int rc;
@@ -324,13 +374,13 @@ int cgs2_kb(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   T* scal = (T*)c->scal;
   const int nb = c->nb;
   hpg::k_dots<T, KB><<<nb, 256, 0, c->stream>>>(Q, ldq, kb, w, n, part);
-  hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(part, nb, 64, kb, scal, 0);
+  hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(part, nb, kb, scal, 0);
   LAUNCH_CHECK();
   c->launches += 2;
   int rc;
   if ((rc = allreduce_scal<T>(c, scal, kb))) return rc;
   hpg::k_cgs_sub_dots<T, KB><<<nb, 256, 0, c->stream>>>(Q, ldq, kb, w, n, scal, part);
-  hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(part, nb, 64, kb, scal + 64, 0);
+  hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(part, nb, kb, scal + 64, 0);
   LAUNCH_CHECK();
   c->launches += 2;
   if ((rc = allreduce_scal<T>(c, scal + 64, kb))) return rc;
@@ -338,7 +388,7 @@ int cgs2_kb(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   LAUNCH_CHECK();
   c->launches += 1;
   if (qnext) {
-    hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(part, nb, 64, 1, scal + 128, c->nranks == 1);
+    hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(part, nb, 1, scal + 128, c->nranks == 1);
     LAUNCH_CHECK();
     c->launches += 1;
     if (c->nranks > 1) {
@@ -346,15 +396,99 @@ int cgs2_kb(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
       hpg::k_sqrt_inplace<T><<<1, 1, 0, c->stream>>>(scal + 128);
       c->launches += 1;
     }
-    hpg::k_scale<T><<<nb, 256, 0, c->stream>>>(w, scal + 128, qnext, n);
+    hpg::k_scale<T><<<grid_for(n), 256, 0, c->stream>>>(w, scal + 128, qnext, n);
     LAUNCH_CHECK();
     c->launches += 1;
   }
   return HPG_OK;
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+  }
+  return fn;
+}
+
+// single-rank CGS2: one cooperative launch (csrc/hpg_cgs.cuh).  The basis is
+// described to the TMA unit as a 2-D tensor [kb rows][n elements] (row pitch
+// ldq), so one tensor copy per tile brings every basis row's segment.
+template <typename T, int KB>
+int cgs2_fused(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
+  hpg::CgsParams<T> p;
+  p.Q = Q;
+  p.w = w;
+  p.qnext = qnext;
+  p.partial = (T*)c->partial;
+  p.scal = (T*)c->scal;
+  p.ldq = ldq;
+  p.n = c->lev[0].n;
+  p.kb = kb;
+  // TMA box: 1 KiB per row (inner extent <= 256 elements); a stage holds
+  // `boxes` boxes so every stage moves ~48 KiB whatever kb is
+  p.box = 1024 / (int)sizeof(T);
+  const size_t budget = 200 * 1024;
+  const size_t row_box = (size_t)(kb + 1) * 1024;
+  p.boxes = (int)std::max<size_t>(1, std::min<size_t>(32, (48 * 1024) / row_box));
+  p.tile = p.boxes * p.box;
+  p.stages = (int)std::min<size_t>(8, budget / (row_box * p.boxes));
+  if (p.stages < 2) return fail(HPG_E_UNSUPPORTED, "basis too wide for the fused CGS2 kernel");
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(HPG_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  const cuuint64_t gdim[2] = {(cuuint64_t)p.n, (cuuint64_t)kb};
+  const cuuint64_t gstride[1] = {(cuuint64_t)ldq * sizeof(T)};
+  const cuuint32_t box[2] = {(cuuint32_t)p.box, (cuuint32_t)kb};
+  const cuuint32_t estride[2] = {1, 1};
+  CUresult cr = enc(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                    (void*)Q, gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(HPG_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  const size_t smem = (size_t)p.stages * (kb + 1) * p.tile * sizeof(T) +
+                      (hpg::kCgsThreads / 32 * KB + KB + 4) * sizeof(T) + 8 * (p.stages + 1) + 16;
+  auto fn = hpg::k_cgs2_fused<T, KB>;
+  CUDA_TRY(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, hpg::kCgsThreads, smem));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int blocks = std::min(std::max(1, per), 8) * sms;
+  void* args[] = {(void*)&p, (void*)&map};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fn, dim3(blocks), dim3(hpg::kCgsThreads), args, smem,
+                                       c->stream));
+  ++c->launches;
+  return HPG_OK;
+}
+
 template <typename T>
 int cgs2_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext, double* out) {
+  if (c->nranks == 1 && c->cgs_fused) {
+    const int kb = k + 1;
+    int rc;
+    {
+      Timed tm(c, M_ORTHO);
+      if (kb <= 4) rc = cgs2_fused<T, 4>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 8) rc = cgs2_fused<T, 8>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 16) rc = cgs2_fused<T, 16>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 32) rc = cgs2_fused<T, 32>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 64) rc = cgs2_fused<T, 64>(c, Q, ldq, kb, w, qnext);
+      else return fail(HPG_E_UNSUPPORTED, "restart basis of %d vectors exceeds 64", kb);
+      if (rc) return rc;
+    }
+    CUDA_TRY(cudaMemcpyAsync(c->pinned, c->scal, 129 * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const T* hv = (const T*)c->pinned;
+    for (int j = 0; j < kb; ++j) {
+      out[j] = (double)hv[j];
+      out[kb + j] = (double)hv[64 + j];
+    }
+    out[2 * kb] = qnext ? (double)hv[128] : 0.0;
+    return HPG_OK;
+  }
   const int kb = k + 1;
   int rc;
   {
@@ -388,7 +522,9 @@ __global__ void k_gemv_combine_y(const T* __restrict__ Q, int64_t ldq, int k, YA
   T yr[KB];
 #pragma unroll
   for (int j = 0; j < KB; ++j) yr[j] = j < k ? (T)y.y[j] : T(0);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  int64_t lo, hi;
+  hpg::block_chunk(n, lo, hi);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     T a = T(0);
 #pragma unroll
     for (int j = 0; j < KB; ++j)
@@ -434,7 +570,7 @@ int build_level(hpg_ctx* c, Level& L, const int dims[3]) {
   L.g = make_geom(dims, c->coords, c->procs);
   L.n = L.g.n;
   L.n_ext = L.n + L.g.halo_size;
-  L.ld = cdiv(std::max<int64_t>(L.n, 1), 64) * 64;
+  L.ld = pad_ld(L.n);
   L.nnz = geom_nnz(L.g);
   if (L.n_ext >= (int64_t)1 << 31) return fail(HPG_E_ARG, "level too large for int32 columns");
   int rc;
@@ -592,9 +728,21 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  {
+    const char* e = getenv("HPG_TAIL_ROWS");
+    c->tail_rows = e ? atoll(e) : (int64_t)2200000;
+    const char* f = getenv("HPG_CGS_FUSED");
+    c->cgs_fused = !(f && f[0] == '0');
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hpg::k_vcycle_tail<double>, 256, 0);
+    c->tail_blocks[0] = std::max(1, per) * sms;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hpg::k_vcycle_tail<float>, 256, 0);
+    c->tail_blocks[1] = std::max(1, per) * sms;
+  }
   c->nb = (int)std::min<int64_t>(8 * sms, std::max<int64_t>(1, cdiv(c->lev[0].n, 256)));
   c->spmv_partial_len = grid_for(c->lev[0].n);
-  if (dmalloc((char**)&c->partial, (size_t)c->nb * 64 * 8, nullptr) ||
+  // partials: [64][grid] for the per-pass kernels (nb CTAs) and the cooperative ones (<= 8 per SM)
+  if (dmalloc((char**)&c->partial, (size_t)std::max(c->nb, 8 * sms) * 64 * 8, nullptr) ||
       dmalloc(&c->spmv_partial, c->spmv_partial_len * 8, nullptr) ||
       dmalloc((char**)&c->scal, 256 * 8, nullptr) || dmalloc((char**)&c->gather, (size_t)nranks * 256 * 8, nullptr))
     return bail(HPG_E_CUDA);
@@ -761,9 +909,9 @@ int hpg_axpy_mixed(hpg_ctx* c, int prec, double* x, const void* z, int64_t n) {
   if (rc || (rc = check_prec(prec))) return rc;
   Timed tm(c, M_VEC);
   if (prec == HPG_F64)
-    hpg::k_axpy_mixed<double><<<c->nb, 256, 0, c->stream>>>(x, (const double*)z, n);
+    hpg::k_axpy_mixed<double><<<grid_for(n), 256, 0, c->stream>>>(x, (const double*)z, n);
   else
-    hpg::k_axpy_mixed<float><<<c->nb, 256, 0, c->stream>>>(x, (const float*)z, n);
+    hpg::k_axpy_mixed<float><<<grid_for(n), 256, 0, c->stream>>>(x, (const float*)z, n);
   LAUNCH_CHECK();
   ++c->launches;
   return HPG_OK;
@@ -779,7 +927,7 @@ int hpg_residual(hpg_ctx* c, const double* b, double* x, double* r, double* rho2
   double* scal = (double*)c->scal;
   const int nbk = grid_for(L.n);
   hpg::k_spmv<double, 1><<<nbk, 256, 0, c->stream>>>(L.cols, L.v64, L.ld, 0, L.n, x, b, r, c->spmv_partial);
-  hpg::k_fold<double><<<1, 1024, 0, c->stream>>>(c->spmv_partial, nbk, 1, 1, scal + 200, 0);
+  hpg::k_fold<double><<<1, 1024, 0, c->stream>>>(c->spmv_partial, nbk, 1, scal + 200, 0);
   LAUNCH_CHECK();
   c->launches += 2;
   if ((rc = allreduce_scal<double>(c, scal + 200, 1))) return rc;
@@ -795,9 +943,9 @@ int hpg_scale_cast(hpg_ctx* c, int prec, const double* r, double rho, void* q0, 
   if (rc || (rc = check_prec(prec))) return rc;
   Timed tm(c, M_VEC);
   if (prec == HPG_F64)
-    hpg::k_scale_cast<double><<<c->nb, 256, 0, c->stream>>>(r, rho, (double*)q0, n);
+    hpg::k_scale_cast<double><<<grid_for(n), 256, 0, c->stream>>>(r, rho, (double*)q0, n);
   else
-    hpg::k_scale_cast<float><<<c->nb, 256, 0, c->stream>>>(r, rho, (float*)q0, n);
+    hpg::k_scale_cast<float><<<grid_for(n), 256, 0, c->stream>>>(r, rho, (float*)q0, n);
   LAUNCH_CHECK();
   ++c->launches;
   return HPG_OK;
@@ -811,7 +959,7 @@ int hpg_sumsq(hpg_ctx* c, int prec, const void* x, int64_t n, double* out) {
   if (prec == HPG_F64) {
     double* scal = (double*)c->scal;
     hpg::k_sumsq<double><<<nb, 256, 0, c->stream>>>((const double*)x, n, (double*)c->partial);
-    hpg::k_fold<double><<<1, 1024, 0, c->stream>>>((const double*)c->partial, nb, 64, 1, scal + 210, 0);
+    hpg::k_fold<double><<<1, 1024, 0, c->stream>>>((const double*)c->partial, nb, 1, scal + 210, 0);
     LAUNCH_CHECK();
     if ((rc = allreduce_scal<double>(c, scal + 210, 1))) return rc;
     CUDA_TRY(cudaMemcpyAsync(c->pinned + 210, scal + 210, 8, cudaMemcpyDeviceToHost, c->stream));
@@ -820,7 +968,7 @@ int hpg_sumsq(hpg_ctx* c, int prec, const void* x, int64_t n, double* out) {
   } else {
     float* scal = (float*)c->scal;
     hpg::k_sumsq<float><<<nb, 256, 0, c->stream>>>((const float*)x, n, (float*)c->partial);
-    hpg::k_fold<float><<<1, 1024, 0, c->stream>>>((const float*)c->partial, nb, 64, 1, scal + 420, 0);
+    hpg::k_fold<float><<<1, 1024, 0, c->stream>>>((const float*)c->partial, nb, 1, scal + 420, 0);
     LAUNCH_CHECK();
     if ((rc = allreduce_scal<float>(c, scal + 420, 1))) return rc;
     CUDA_TRY(cudaMemcpyAsync(c->pinned + 210, scal + 420, 4, cudaMemcpyDeviceToHost, c->stream));
@@ -851,6 +999,14 @@ int hpg_allreduce_host(hpg_ctx* c, double* vals, int n) {
 }
 
 int64_t hpg_launch_count(hpg_ctx* c) { return c ? c->launches : -1; }
+
+int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
+  if (!c || !key) return fail(HPG_E_ARG, "null argument");
+  if (!strcmp(key, "cgs_fused")) c->cgs_fused = value != 0;
+  else if (!strcmp(key, "tail_rows")) c->tail_rows = value;
+  else return fail(HPG_E_ARG, "unknown option %s", key);
+  return HPG_OK;
+}
 
 // mode 1: enable, 0: disable, 2: synchronise, add each motif's seconds into
 // seconds[6] (GS, SpMV, Ortho, Restriction, Prolongation, Vector ops) and reset.

@@ -1,0 +1,76 @@
+// Persistent cooperative kernel for the coarse end of the V-cycle.
+//
+// Below a size threshold a GS color pass is a few microseconds of HBM/L2
+// traffic but still pays a full dependent-launch gap; at 256^3 the three
+// coarse levels are 40 of the ~58 launches of a V-cycle.  This kernel runs
+// the whole V-cycle tail (levels lc .. L-1: pre-smooth, restrict, recurse,
+// prolong, post-smooth; ref: multigrid.py:140-171) in ONE cooperative launch,
+// one grid-wide barrier between dependent phases instead of one launch.
+// Arithmetic per row is the same device function the per-pass kernels use,
+// so results are bitwise identical; vector loads go through L2 (ld.global.cg)
+// because other blocks wrote them earlier in the same launch.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "hpg_kernels.cuh"
+
+namespace hpg {
+
+template <typename T>
+struct TailLevel {
+  const int32_t* cols;
+  const T* vals;
+  const int32_t* inj;  // dst map into this level from its parent (unused for the first)
+  T* z;
+  T* r;
+  int64_t ld, n, n_ext;
+  int64_t off[9];
+  int ncolors;
+};
+
+constexpr int kMaxTail = 8;
+
+template <typename T>
+struct TailParams {
+  TailLevel<T> lv[kMaxTail];
+  int nl, nu1, nu2, nu_c;
+};
+
+template <typename T>
+__device__ __forceinline__ void tail_sweep(const TailLevel<T>& L, bool zero, int64_t gt, int64_t gs,
+                                           cooperative_groups::grid_group& grid) {
+  if (zero) {
+    for (int64_t i = gt; i < L.n_ext; i += gs) L.z[i] = T(0);
+    grid.sync();
+  }
+  for (int c = 0; c < L.ncolors; ++c) {
+    for (int64_t i = L.off[c] + gt; i < L.off[c + 1]; i += gs) gs_row<T, true>(L.cols, L.vals, L.ld, i, L.r, L.z);
+    grid.sync();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 2) k_vcycle_tail(const __grid_constant__ TailParams<T> p) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+  for (int l = 0; l < p.nl; ++l) {
+    const TailLevel<T>& L = p.lv[l];
+    const bool last = l == p.nl - 1;
+    const int sweeps = last ? p.nu_c : p.nu1;
+    for (int s = 0; s < sweeps; ++s) tail_sweep(L, s == 0, gt, gs, grid);
+    if (last) break;
+    const TailLevel<T>& C = p.lv[l + 1];
+    for (int64_t j = gt; j < C.n; j += gs) restrict_row<T, true>(L.cols, L.vals, L.ld, j, C.inj, L.r, L.z, C.r);
+    grid.sync();
+  }
+  for (int l = p.nl - 2; l >= 0; --l) {
+    const TailLevel<T>& L = p.lv[l];
+    const TailLevel<T>& C = p.lv[l + 1];
+    for (int64_t j = gt; j < C.n; j += gs) L.z[j] = add_rn(__ldcg(L.z + j), __ldcg(C.z + C.inj[j]));
+    grid.sync();
+    for (int s = 0; s < p.nu2; ++s) tail_sweep(L, false, gt, gs, grid);
+  }
+}
+
+}  // namespace hpg

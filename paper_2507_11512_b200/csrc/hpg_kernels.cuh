@@ -32,41 +32,78 @@ __device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(
 // evict first from L2 so the gathered vectors stay resident
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
   int32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ float ld_stream(const float* p) {
   float v;
-  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ double ld_stream(const double* p) {
   double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 
 // ------------------------------------------------------------ stencil kernels
+//
+// Every stencil kernel handles one row per thread and is written "all loads
+// first": the 27 column indices and 27 values of the row are loaded into
+// registers, then the 27 gathers are issued, then the products are summed in
+// slot order.  That puts ~81 independent loads in flight per thread, which
+// saturates HBM at modest occupancy on the big levels and turns the small
+// (coarse) levels into ~2 memory round trips instead of 27.
+
+// acc = sum_s vals[s] * x[col[s]] with the diagonal slot's value returned in
+// *d and (when ZERO_DIAG) excluded as 0 * x[i], exactly like the reference's
+// zeroed offvals (ref: smoother.py:44-46, 62-66).
+// Vector loads that must see writes made by OTHER blocks earlier in the same
+// kernel (the persistent coarse-level kernel): bypass L1 (ld.global.cg).
+template <bool COHERENT, typename T>
+__device__ __forceinline__ T ldv(const T* p) {
+  if (COHERENT) return __ldcg(p);
+  return *p;
+}
+
+template <typename T, bool ZERO_DIAG, bool COHERENT = false>
+__device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+                                            int64_t ld, int64_t i, const T* x, T* d) {
+  int32_t c[27];
+  T v[27];
+#pragma unroll
+  for (int s = 0; s < 27; ++s) c[s] = ld_stream(cols + s * ld + i);
+#pragma unroll
+  for (int s = 0; s < 27; ++s) v[s] = ld_stream(vals + s * ld + i);
+  T g[27];
+#pragma unroll
+  for (int s = 0; s < 27; ++s) g[s] = ldv<COHERENT>(x + (c[s] < 0 ? ~c[s] : c[s]));
+  T acc = T(0);
+#pragma unroll
+  for (int s = 0; s < 27; ++s) {
+    T vs = v[s];
+    if (ZERO_DIAG && c[s] < 0) {
+      *d = vs;
+      vs = T(0);
+    }
+    acc = add_rn(acc, mul_rn(vs, g[s]));
+  }
+  return acc;
+}
 
 // y[i] = sum_s A[i,s] x[col[i,s]]  for rows [row0, row0+nrows)
 // MODE 0: y = Ax.  MODE 1: y = b - Ax and per-block partial of sum y^2 (fp64 outer residual).
 template <typename T, int MODE>
-__global__ void __launch_bounds__(256) k_spmv(const int32_t* __restrict__ cols, const T* __restrict__ vals,
-                                              int64_t ld, int64_t row0, int64_t nrows,
-                                              const T* __restrict__ x, const T* __restrict__ b,
-                                              T* __restrict__ y, double* __restrict__ partial) {
+__global__ void __launch_bounds__(256, 2) k_spmv(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+                                                 int64_t ld, int64_t row0, int64_t nrows,
+                                                 const T* __restrict__ x, const T* __restrict__ b,
+                                                 T* __restrict__ y, double* __restrict__ partial) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double sq = 0.0;
   if (t < nrows) {
     const int64_t i = row0 + t;
-    T acc = T(0);
-#pragma unroll
-    for (int s = 0; s < 27; ++s) {
-      int32_t c = ld_stream(cols + s * ld + i);
-      const T v = ld_stream(vals + s * ld + i);
-      c = c < 0 ? ~c : c;
-      acc = add_rn(acc, mul_rn(v, x[c]));
-    }
+    T dd;
+    const T acc = row_accumulate<T, false>(cols, vals, ld, i, x, &dd);
     if (MODE == 0) {
       y[i] = acc;
     } else {
@@ -92,49 +129,42 @@ __global__ void __launch_bounds__(256) k_spmv(const int32_t* __restrict__ cols, 
 
 // One color pass of forward Gauss-Seidel over rows [row0, row0+nrows):
 //   z_i = (r_i - sum_{s != diag} A[i,s] z[col]) / a_ii
-// The diagonal slot contributes 0 * z_i exactly like the reference's zeroed
-// offvals (ref: smoother.py:44-46, 62-66).
+template <typename T, bool COHERENT = false>
+__device__ __forceinline__ void gs_row(const int32_t* __restrict__ cols, const T* __restrict__ vals, int64_t ld,
+                                       int64_t i, const T* __restrict__ r, T* z) {
+  T d = T(0);
+  const T acc = row_accumulate<T, true, COHERENT>(cols, vals, ld, i, z, &d);
+  z[i] = div_rn(sub_rn(ldv<COHERENT>(r + i), acc), d);
+}
+
 template <typename T>
-__global__ void __launch_bounds__(256) k_gs_pass(const int32_t* __restrict__ cols, const T* __restrict__ vals,
-                                                 int64_t ld, int64_t row0, int64_t nrows,
-                                                 const T* __restrict__ r, T* z) {
+__global__ void __launch_bounds__(256, 2) k_gs_pass(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+                                                    int64_t ld, int64_t row0, int64_t nrows,
+                                                    const T* __restrict__ r, T* z) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nrows) return;
-  const int64_t i = row0 + t;
-  T acc = T(0);
-  T d = T(0);
-#pragma unroll
-  for (int s = 0; s < 27; ++s) {
-    int32_t c = ld_stream(cols + s * ld + i);
-    T v = ld_stream(vals + s * ld + i);
-    if (c < 0) {
-      d = v;
-      v = T(0);
-      c = ~c;
-    }
-    acc = add_rn(acc, mul_rn(v, z[c]));
-  }
-  z[i] = div_rn(sub_rn(r[i], acc), d);
+  gs_row<T>(cols, vals, ld, row0 + t, r, z);
 }
 
 // Fused residual + injection: for fine color-0 row j < nc,
 //   rc[dst[j]] = r[j] - (A z)[j]     (ref: multigrid.py:107-128)
+template <typename T, bool COHERENT = false>
+__device__ __forceinline__ void restrict_row(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+                                             int64_t ld, int64_t j, const int32_t* __restrict__ dst,
+                                             const T* __restrict__ r, const T* z, T* __restrict__ rc) {
+  T dd;
+  const T acc = row_accumulate<T, false, COHERENT>(cols, vals, ld, j, z, &dd);
+  rc[dst[j]] = sub_rn(ldv<COHERENT>(r + j), acc);
+}
+
 template <typename T>
-__global__ void __launch_bounds__(256) k_restrict(const int32_t* __restrict__ cols, const T* __restrict__ vals,
-                                                  int64_t ld, int64_t nc, const int32_t* __restrict__ dst,
-                                                  const T* __restrict__ r, const T* __restrict__ z,
-                                                  T* __restrict__ rc) {
+__global__ void __launch_bounds__(256, 2) k_restrict(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+                                                     int64_t ld, int64_t nc, const int32_t* __restrict__ dst,
+                                                     const T* __restrict__ r, const T* __restrict__ z,
+                                                     T* __restrict__ rc) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nc) return;
-  T acc = T(0);
-#pragma unroll
-  for (int s = 0; s < 27; ++s) {
-    int32_t c = ld_stream(cols + s * ld + j);
-    const T v = ld_stream(vals + s * ld + j);
-    c = c < 0 ? ~c : c;
-    acc = add_rn(acc, mul_rn(v, z[c]));
-  }
-  rc[dst[j]] = sub_rn(r[j], acc);
+  restrict_row<T>(cols, vals, ld, j, dst, r, z, rc);
 }
 
 // Injection transpose: z[j] += zc[dst[j]]  (ref: multigrid.py:131-137)
@@ -159,8 +189,11 @@ __global__ void k_pack(const T* __restrict__ v, const int32_t* __restrict__ idx,
 // Deterministic two-stage reductions: every kernel writes one partial per
 // block (fixed grid), a single-block fold sums them in a fixed tree order.
 
+// Partials are stored j-major: partial[j * nb + block], so the fold reads
+// them coalesced.  Each block owns one contiguous chunk of rows (good DRAM
+// page locality for the kb concurrent Q streams).
 template <int KB, typename T>
-__device__ __forceinline__ void block_reduce_store(T (&acc)[KB], int kb, T* out) {
+__device__ __forceinline__ void block_reduce_store(T (&acc)[KB], int kb, T* out, int nb) {
   __shared__ T red[8][KB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -174,28 +207,37 @@ __device__ __forceinline__ void block_reduce_store(T (&acc)[KB], int kb, T* out)
   if (threadIdx.x < kb) {
     T a = red[0][threadIdx.x];
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) a += red[w][threadIdx.x];
-    out[threadIdx.x] = a;
+    out[(int64_t)threadIdx.x * nb + blockIdx.x] = a;
   }
 }
 
-// partial[b][j] = sum_{i in block b} Q[j][i] * w[i],  j < kb
+// rows of block b: [lo, hi)
+__device__ __forceinline__ void block_chunk(int64_t n, int64_t& lo, int64_t& hi) {
+  const int64_t chunk = ((n + gridDim.x - 1) / gridDim.x + 31) & ~(int64_t)31;
+  lo = (int64_t)blockIdx.x * chunk;
+  hi = lo + chunk < n ? lo + chunk : n;
+}
+
+// partial[j][b] = sum_{i in chunk b} Q[j][i] * w[i],  j < kb
 template <typename T, int KB>
 __global__ void __launch_bounds__(256) k_dots(const T* __restrict__ Q, int64_t ldq, int kb,
                                               const T* __restrict__ w, int64_t n, T* __restrict__ partial) {
   T acc[KB];
 #pragma unroll
   for (int j = 0; j < KB; ++j) acc[j] = T(0);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  int64_t lo, hi;
+  block_chunk(n, lo, hi);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const T wi = w[i];
 #pragma unroll
     for (int j = 0; j < KB; ++j)
       if (j < kb) acc[j] = fma(Q[j * ldq + i], wi, acc[j]);
   }
-  block_reduce_store<KB>(acc, kb, partial + (int64_t)blockIdx.x * 64);
+  block_reduce_store<KB>(acc, kb, partial, gridDim.x);
 }
 
 // CGS pass-1 correction fused with the pass-2 projection:
-//   w_i -= sum_j Q[j][i] h[j];  partial[b][j] = sum Q[j][i] w_i(new)
+//   w_i -= sum_j Q[j][i] h[j];  partial[j][b] = sum Q[j][i] w_i(new)
 template <typename T, int KB>
 __global__ void __launch_bounds__(256) k_cgs_sub_dots(const T* __restrict__ Q, int64_t ldq, int kb,
                                                       T* __restrict__ w, int64_t n, const T* __restrict__ h,
@@ -206,7 +248,9 @@ __global__ void __launch_bounds__(256) k_cgs_sub_dots(const T* __restrict__ Q, i
     acc[j] = T(0);
     hr[j] = j < kb ? h[j] : T(0);
   }
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  int64_t lo, hi;
+  block_chunk(n, lo, hi);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     T q[KB];
 #pragma unroll
     for (int j = 0; j < KB; ++j) q[j] = j < kb ? Q[j * ldq + i] : T(0);
@@ -220,7 +264,7 @@ __global__ void __launch_bounds__(256) k_cgs_sub_dots(const T* __restrict__ Q, i
     for (int j = 0; j < KB; ++j)
       if (j < kb) acc[j] = fma(q[j], wi, acc[j]);
   }
-  block_reduce_store<KB>(acc, kb, partial + (int64_t)blockIdx.x * 64);
+  block_reduce_store<KB>(acc, kb, partial, gridDim.x);
 }
 
 // CGS pass-2 correction fused with the norm: w_i -= sum_j Q[j][i] h[j]; partial[b] = sum w_i^2
@@ -232,7 +276,9 @@ __global__ void __launch_bounds__(256) k_cgs_sub_norm(const T* __restrict__ Q, i
 #pragma unroll
   for (int j = 0; j < KB; ++j) hr[j] = j < kb ? h[j] : T(0);
   T acc[1] = {T(0)};
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  int64_t lo, hi;
+  block_chunk(n, lo, hi);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     T tsum = T(0);
 #pragma unroll
     for (int j = 0; j < KB; ++j)
@@ -241,22 +287,34 @@ __global__ void __launch_bounds__(256) k_cgs_sub_norm(const T* __restrict__ Q, i
     w[i] = wi;
     acc[0] = fma(wi, wi, acc[0]);
   }
-  block_reduce_store<1>(acc, 1, partial + (int64_t)blockIdx.x * 64);
+  block_reduce_store<1>(acc, 1, partial, gridDim.x);
 }
 
-// Single-block fold of nb partial rows (row stride `stride`) into out[j], j < kb.
-// One warp per output, lanes stride over the blocks, fixed shuffle tree:
-// the same bits on every run.
+// Single-block fold of j-major partials [kb][nb] into out[j], fixed order.
+// kb == 1: all threads stride over the blocks, then a shared-memory tree;
+// kb > 1: one warp per output, lanes stride, shuffle tree.
 template <typename T>
-__global__ void k_fold(const T* __restrict__ partial, int nb, int stride, int kb, T* __restrict__ out,
-                       int do_sqrt) {
+__global__ void k_fold(const T* __restrict__ partial, int nb, int kb, T* __restrict__ out, int do_sqrt) {
+  if (kb == 1) {
+    __shared__ T red[1024];
+    T a = T(0);
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) a += partial[b];
+    red[threadIdx.x] = a;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+      if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = do_sqrt ? sqrt(red[0]) : red[0];
+    return;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int j = warp; j < kb; j += nw) {
     T a = T(0);
-    for (int b = lane; b < nb; b += 32) a += partial[(int64_t)b * stride + j];
+    for (int b = lane; b < nb; b += 32) a += partial[(int64_t)j * nb + b];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) out[j] = do_sqrt ? sqrt(a) : a;
+    if (lane == 0) out[j] = a;
   }
 }
 
@@ -278,48 +336,34 @@ __global__ void k_sqrt_inplace(T* v) {
 // Q[k+1] = w / beta  (0 when beta == 0)  (ref: krylov.py:267-273)
 template <typename T>
 __global__ void k_scale(const T* __restrict__ w, const T* __restrict__ beta, T* __restrict__ q, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
   const T bt = *beta;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    q[i] = bt != T(0) ? div_rn(w[i], bt) : T(0);
+  q[i] = bt != T(0) ? div_rn(w[i], bt) : T(0);
 }
 
 // Q0 = (T)(r / rho) computed in fp64 then narrowed (ref: krylov.py:250-252)
 template <typename T>
 __global__ void k_scale_cast(const double* __restrict__ r, double rho, T* __restrict__ q, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    q[i] = (T)__ddiv_rn(r[i], rho);
-}
-
-// out[i] = sum_{j<k} Q[j][i] y[j]   (ref: krylov.py:288-289)
-template <typename T, int KB>
-__global__ void __launch_bounds__(256) k_gemv_combine(const T* __restrict__ Q, int64_t ldq, int k,
-                                                      const T* __restrict__ y, T* __restrict__ out, int64_t n) {
-  T yr[KB];
-#pragma unroll
-  for (int j = 0; j < KB; ++j) yr[j] = j < k ? y[j] : T(0);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    T a = T(0);
-#pragma unroll
-    for (int j = 0; j < KB; ++j)
-      if (j < k) a = fma(Q[j * ldq + i], yr[j], a);
-    out[i] = a;
-  }
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) q[i] = (T)__ddiv_rn(r[i], rho);
 }
 
 // x += z (fp64 += promoted z)   (ref: krylov.py:292-293)
 template <typename T>
 __global__ void k_axpy_mixed(double* __restrict__ x, const T* __restrict__ z, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    x[i] = __dadd_rn(x[i], (double)z[i]);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = __dadd_rn(x[i], (double)z[i]);
 }
 
 // partial sum of x^2 (norms of b and of arbitrary vectors)
 template <typename T>
 __global__ void __launch_bounds__(256) k_sumsq(const T* __restrict__ x, int64_t n, T* __restrict__ partial) {
   T acc[1] = {T(0)};
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    acc[0] = fma(x[i], x[i], acc[0]);
-  block_reduce_store<1>(acc, 1, partial + (int64_t)blockIdx.x * 64);
+  int64_t lo, hi;
+  block_chunk(n, lo, hi);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) acc[0] = fma(x[i], x[i], acc[0]);
+  block_reduce_store<1>(acc, 1, partial, gridDim.x);
 }
 
 // -------------------------------------------------------------- setup

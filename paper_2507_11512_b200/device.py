@@ -53,6 +53,9 @@ class Context:
         self.call("hpg_timers", mode, out.ctypes.data_as(C.POINTER(C.c_double)))
         return out
 
+    def set_option(self, key, value):
+        self.call("hpg_set_option", key.encode(), int(value))
+
     def sync(self):
         self.call("hpg_sync")
 

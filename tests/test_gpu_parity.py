@@ -204,3 +204,34 @@ def test_large_grid_properties():
     res, x = _solve(128, "mixed")
     assert res.converged and res.relres < 1e-9
     assert np.max(np.abs(x - 1.0)) < 1e-4
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_fused_cgs2_matches_per_pass_kernels(dt):
+    """The cooperative bulk-copy CGS2 and the per-pass kernels orthogonalise alike
+    (same arithmetic per element, reductions differ only in grouping)."""
+    import ctypes as C
+    from paper_2507_11512_b200 import _lib
+    from paper_2507_11512_b200.krylov import GmresWorkspace
+    h = _hier(32, 2)
+    ctx = h.ctx
+    n = h.levels[0].A_hi.n_rows
+    npdt = np.float32 if dt == "f32" else np.float64
+    tdt = torch.float32 if dt == "f32" else torch.float64
+    prec = _lib.F32 if dt == "f32" else _lib.F64
+    tol = 2e-5 if dt == "f32" else 1e-12
+    for k in (0, 5, 29):
+        outs = []
+        for fused in (1, 0):
+            ctx.set_option("cgs_fused", fused)
+            ws = GmresWorkspace.allocate(n, 30, npdt, device="cuda")
+            g = torch.Generator(device="cuda").manual_seed(k)
+            ws.Q.copy_(torch.randn(ws.Q.shape, generator=g, device="cuda", dtype=tdt))
+            w = torch.randn(n, generator=g, device="cuda", dtype=tdt)
+            res = np.zeros(2 * (k + 1) + 1)
+            ctx.call("hpg_cgs2", prec, _lib.ptr(ws.Q), ws.Q.stride(0), k, _lib.ptr(w),
+                     _lib.ptr(ws.Q[k + 1]), res.ctypes.data_as(C.POINTER(C.c_double)))
+            outs.append((res, ws.Q[k + 1].cpu().numpy()))
+        np.testing.assert_allclose(outs[0][0], outs[1][0], rtol=tol, atol=tol)
+        np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=0, atol=tol)
+    h.close()

@@ -1,0 +1,98 @@
+"""Per-component CUDA-event timings at L^3 (warm, repeated).  Not a bench number:
+used to tune kernels between bench runs.  Prints one JSON dict."""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--local", type=int, default=256)
+    p.add_argument("--reps", type=int, default=20)
+    a = p.parse_args()
+    import torch
+    from paper_2507_11512_b200 import _lib
+    from paper_2507_11512_b200.bench import BenchConfig, _build_state, _solve
+    from paper_2507_11512_b200.krylov import GmresWorkspace
+    cfg = BenchConfig(local_nx=a.local, local_ny=a.local, local_nz=a.local, time_seconds=0)
+    hier, lv, b = _build_state(cfg, 1, None, 0)
+    ctx = hier.ctx
+    st = ctx.stream
+    n, ne = lv.A_hi.n_rows, lv.A_hi.n_cols_extended
+    nnz = lv.A_hi.nnz_total
+    out = {"local": a.local, "tail_rows": os.environ.get("HPG_TAIL_ROWS", "default")}
+
+    def timeit(fn, reps=a.reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps * 1e3  # us
+
+    x32 = torch.randn(ne, device="cuda", dtype=torch.float32)
+    y32 = torch.empty(n, device="cuda", dtype=torch.float32)
+    r32 = torch.randn(n, device="cuda", dtype=torch.float32)
+    z32 = torch.zeros(ne, device="cuda", dtype=torch.float32)
+    us = timeit(lambda: ctx.call("hpg_spmv", 0, _lib.F32, _lib.ptr(x32), _lib.ptr(y32)))
+    out["spmv_f32_us"] = us
+    out["spmv_f32_GBs"] = (nnz * 8 + 2 * n * 4) / us / 1e3
+    x64 = torch.randn(ne, device="cuda", dtype=torch.float64)
+    r64 = torch.empty(n, device="cuda", dtype=torch.float64)
+    b64 = torch.randn(n, device="cuda", dtype=torch.float64)
+    rho = C.c_double()
+    us = timeit(lambda: ctx.call("hpg_residual", _lib.ptr(b64), _lib.ptr(x64), _lib.ptr(r64), C.byref(rho)))
+    out["residual_f64_us"] = us
+    out["residual_f64_GBs"] = (nnz * 12 + 3 * n * 8) / us / 1e3
+    us = timeit(lambda: ctx.call("hpg_gs_sweep", 0, _lib.F32, _lib.ptr(r32), _lib.ptr(z32), 0))
+    out["gs_sweep_L0_f32_us"] = us
+    out["gs_sweep_L0_f32_GBs"] = (nnz * 8 + 3 * n * 4) / us / 1e3
+    us = timeit(lambda: hier.apply(r32, out=z32))
+    out["vcycle_f32_us"] = us
+    us = timeit(lambda: hier.apply(r64 if False else b64, out=x64))
+    out["vcycle_f64_us"] = us
+    # model bytes of one V-cycle (f32)
+    from paper_2507_11512_b200.metrics import Tally
+    from paper_2507_11512_b200.multigrid import count_vcycle
+    t = Tally()
+    count_vcycle(hier, t, np.float32)
+    out["vcycle_f32_model_GBs"] = t.total_bytes() / out["vcycle_f32_us"] / 1e3
+    ws = GmresWorkspace.allocate(n, 30, np.float32, device="cuda")
+    ws.Q.normal_()
+    w = torch.randn(n, device="cuda", dtype=torch.float32)
+    res = np.zeros(64)
+    for k in (0, 7, 15, 29):
+        us = timeit(lambda: ctx.call("hpg_cgs2", _lib.F32, _lib.ptr(ws.Q), ws.Q.stride(0), k, _lib.ptr(w),
+                                     _lib.ptr(ws.Q[k + 1]), res.ctypes.data_as(C.POINTER(C.c_double))), reps=5)
+        kb = k + 1
+        out[f"cgs2_k{kb}_us"] = us
+        out[f"cgs2_k{kb}_modelGBs"] = (4 * n * kb * 4 + 4 * n * 4 + 3 * n * 4) / us / 1e3
+    # one restart cycle of the real solve
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _solve(cfg, hier, lv, b, None, 0, "mixed", 1e-9, 30)
+    tal = Tally()
+    e0.record(st)
+    res_ = _solve(cfg, hier, lv, b, None, 0, "mixed", 1e-9, 30, tal)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    out["solve30_ms"] = ms
+    out["solve30_model_GBs"] = tal.total_bytes() / ms / 1e6
+    out["solve30_GFs"] = tal.total_flops() / ms / 1e6
+    out["solve30_motif_s"] = tal.seconds
+    print(json.dumps(out))
+    hier.close()
+
+
+if __name__ == "__main__":
+    main()
