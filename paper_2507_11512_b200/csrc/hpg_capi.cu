@@ -1,7 +1,5 @@
 // libhpgmxp.so: context, hierarchy build, and the extern "C" entry points
 // declared in include/hpgmxp.h.
-#include <cuda.h>
-#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -403,21 +401,8 @@ int cgs2_kb(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   return HPG_OK;
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      fn = nullptr;
-  }
-  return fn;
-}
-
-// single-rank CGS2: one cooperative launch (csrc/hpg_cgs.cuh).  The basis is
-// described to the TMA unit as a 2-D tensor [kb rows][n elements] (row pitch
-// ldq), so one tensor copy per tile brings every basis row's segment.
-template <typename T, int KB>
+// single-rank CGS2: one cooperative launch (csrc/hpg_cgs.cuh)
+template <typename T, int WR, int RPW, int U>
 int cgs2_fused(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   hpg::CgsParams<T> p;
   p.Q = Q;
@@ -428,54 +413,33 @@ int cgs2_fused(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   p.ldq = ldq;
   p.n = c->lev[0].n;
   p.kb = kb;
-  // TMA box: 1 KiB per row (inner extent <= 256 elements); a stage holds
-  // `boxes` boxes so every stage moves ~48 KiB whatever kb is
-  p.box = 1024 / (int)sizeof(T);
-  const size_t budget = 200 * 1024;
-  const size_t row_box = (size_t)(kb + 1) * 1024;
-  p.boxes = (int)std::max<size_t>(1, std::min<size_t>(32, (48 * 1024) / row_box));
-  p.tile = p.boxes * p.box;
-  p.stages = (int)std::min<size_t>(8, budget / (row_box * p.boxes));
-  if (p.stages < 2) return fail(HPG_E_UNSUPPORTED, "basis too wide for the fused CGS2 kernel");
-  auto enc = tensor_map_encoder();
-  if (!enc) return fail(HPG_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-  CUtensorMap map;
-  const cuuint64_t gdim[2] = {(cuuint64_t)p.n, (cuuint64_t)kb};
-  const cuuint64_t gstride[1] = {(cuuint64_t)ldq * sizeof(T)};
-  const cuuint32_t box[2] = {(cuuint32_t)p.box, (cuuint32_t)kb};
-  const cuuint32_t estride[2] = {1, 1};
-  CUresult cr = enc(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                    (void*)Q, gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return fail(HPG_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
-  const size_t smem = (size_t)p.stages * (kb + 1) * p.tile * sizeof(T) +
-                      (hpg::kCgsThreads / 32 * KB + KB + 4) * sizeof(T) + 8 * (p.stages + 1) + 16;
-  auto fn = hpg::k_cgs2_fused<T, KB>;
-  CUDA_TRY(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (ldq % 32) return fail(HPG_E_ARG, "basis row stride must be a multiple of 32 elements");
+  auto fn = hpg::k_cgs2_fused<T, WR, RPW, U>;
   int per = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, hpg::kCgsThreads, smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, hpg::kCgsThreads, 0));
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   const int blocks = std::min(std::max(1, per), 8) * sms;
-  void* args[] = {(void*)&p, (void*)&map};
-  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fn, dim3(blocks), dim3(hpg::kCgsThreads), args, smem,
-                                       c->stream));
+  void* args[] = {(void*)&p};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fn, dim3(blocks), dim3(hpg::kCgsThreads), args, 0, c->stream));
   ++c->launches;
   return HPG_OK;
 }
 
 template <typename T>
 int cgs2_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext, double* out) {
-  if (c->nranks == 1 && c->cgs_fused) {
+  if (c->nranks == 1 && c->cgs_fused && c->lev[0].n % (16 / (int)sizeof(T)) == 0) {
     const int kb = k + 1;
     int rc;
     {
       Timed tm(c, M_ORTHO);
-      if (kb <= 4) rc = cgs2_fused<T, 4>(c, Q, ldq, kb, w, qnext);
-      else if (kb <= 8) rc = cgs2_fused<T, 8>(c, Q, ldq, kb, w, qnext);
-      else if (kb <= 16) rc = cgs2_fused<T, 16>(c, Q, ldq, kb, w, qnext);
-      else if (kb <= 32) rc = cgs2_fused<T, 32>(c, Q, ldq, kb, w, qnext);
-      else if (kb <= 64) rc = cgs2_fused<T, 64>(c, Q, ldq, kb, w, qnext);
+      if (kb <= 1) rc = cgs2_fused<T, 1, 1, 8>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 2) rc = cgs2_fused<T, 2, 1, 8>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 4) rc = cgs2_fused<T, 4, 1, 8>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 8) rc = cgs2_fused<T, 4, 2, 4>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 16) rc = cgs2_fused<T, 8, 2, 4>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 32) rc = cgs2_fused<T, 8, 4, 2>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 64) rc = cgs2_fused<T, 8, 8, 1>(c, Q, ldq, kb, w, qnext);
       else return fail(HPG_E_UNSUPPORTED, "restart basis of %d vectors exceeds 64", kb);
       if (rc) return rc;
     }

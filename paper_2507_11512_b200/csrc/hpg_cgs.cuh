@@ -1,108 +1,93 @@
-// CGS2 + norm + normalise in ONE persistent cooperative kernel, with the
-// basis rows streamed through shared memory by the bulk-copy (TMA) engine.
+// CGS2 + norm + normalise in ONE persistent cooperative kernel.
 //
 // One Arnoldi step needs, for kb = k+1 basis rows Q[0..kb) of length n
 // (ref: krylov.py:110-129, 266-273):
 //   pass A  h1 = Q w                  (kb dots)
 //   pass B  w -= Q^T h1 ; h2 = Q w    (correction fused with the 2nd projection)
 //   pass C  w -= Q^T h2 ; beta^2 = w.w
-//   pass D  Q[k] = w / beta
+//   pass D  Q[k+1] = w / beta
 // i.e. three streams of the kb rows instead of the four of the textbook
-// order.  Each pass walks this CTA's contiguous range of tiles; thread 0
-// issues cp.async.bulk copies of the kb row-segments (and w) of tile t+S-1
-// into stage (t+S-1)%S while all threads consume tile t from shared memory,
-// so the copy engine keeps ~S-1 tiles of every row in flight with no
-// register cost.  Between passes one grid barrier, a fixed-order fold of the
-// per-CTA partials by CTA 0, and another barrier: deterministic, and no host
-// round trip until the final (h1, h2, beta) read.
+// order, and one launch instead of ~8.
+//
+// Data movement: the CTA's 8 warps are WR row groups x WE element groups.
+// Row group rg streams rows rg, rg+WR, ...; element group eg takes its own
+// tiles; every lane moves 16-byte vectors, U tiles at a time, so a lane has
+// U*(rows/WR + 1) independent 16 B loads in flight and a warp reads 512
+// contiguous bytes of a row per load.  Small bases (kb < 8) use fewer row
+// groups so every warp still streams.  (A first version staged
+// the rows through shared memory with cp.async.bulk / 2-D TMA copies; its
+// per-tile mbarrier round trip capped it near 3.6 TB/s.)  The correction
+// sum_j Q[j][i] h[j] of passes B/C crosses the row group: each warp writes
+// its partial for the tile to shared memory and every warp of the group adds
+// the WR partials in warp order, so w_i is identical (and deterministic).
+// Between passes: grid barrier, fixed-order fold of the per-CTA partials by
+// CTA 0, grid barrier.
 #pragma once
 #include <cooperative_groups.h>
-#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace hpg {
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-// 1-D bulk copy global -> shared, completion counted on an mbarrier
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  using V = float4;
+  static constexpr int N = 4;
+};
+template <>
+struct Vec16<double> {
+  using V = double2;
+  static constexpr int N = 2;
+};
 
-// 2-D tensor copy: box {tile, kb} of the basis at element (x, y) -> shared
-__device__ __forceinline__ void tma_2d_g2s(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"((uint64_t)map), "r"(x), "r"(y), "r"(smem_u32(bar))
-      : "memory");
+template <typename T>
+__device__ __forceinline__ T vget(const typename Vec16<T>::V& v, int c);
+template <>
+__device__ __forceinline__ float vget<float>(const float4& v, int c) {
+  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+template <>
+__device__ __forceinline__ double vget<double>(const double2& v, int c) {
+  return c == 0 ? v.x : v.y;
+}
+template <typename T>
+__device__ __forceinline__ void vset(typename Vec16<T>::V& v, int c, T x);
+template <>
+__device__ __forceinline__ void vset<float>(float4& v, int c, float x) {
+  if (c == 0) v.x = x;
+  else if (c == 1) v.y = x;
+  else if (c == 2) v.z = x;
+  else v.w = x;
+}
+template <>
+__device__ __forceinline__ void vset<double>(double2& v, int c, double x) {
+  if (c == 0) v.x = x;
+  else v.y = x;
 }
 
 template <typename T>
 struct CgsParams {
-  const T* Q;      // basis, row-major, row stride ldq
+  const T* Q;      // basis, row-major, row stride ldq (multiple of 32 elements)
   T* w;            // vector being orthogonalised (length >= round_up(n, 32))
+                   // n must be a multiple of the 16-byte vector width (host checks)
   T* qnext;        // Q[k+1] (NULL: skip norm/normalise)
-  T* partial;      // [KBMAX][gridDim] per-CTA partials
+  T* partial;      // [64][gridDim] per-CTA partials
   T* scal;         // [0,64) h1, [64,128) h2, [128] beta
   int64_t ldq, n;
-  int kb, tile;    // elements per tile = boxes * box
-  int box, boxes;  // TMA box inner extent (elements) and boxes per stage
-  int stages;
+  int kb;
 };
 
-constexpr int kCgsThreads = 512;
-
-template <typename T, int KB>
-__device__ __forceinline__ void cgs_block_reduce(T (&acc)[KB], int kb, T* out, T* red) {
-  // red: [kCgsThreads/32][KB] in shared memory
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int j = 0; j < KB; ++j) {
-    T a = acc[j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) red[warp * KB + j] = a;
-  }
-  __syncthreads();
-  if (threadIdx.x < kb) {
-    T a = T(0);
-    for (int w = 0; w < kCgsThreads / 32; ++w) a += red[w * KB + threadIdx.x];
-    out[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = a;
-  }
-  __syncthreads();
-}
+constexpr int kCgsThreads = 256;
+constexpr int kCgsWarps = kCgsThreads / 32;
 
 // CTA 0 folds the per-CTA partials of cnt outputs into dst (fixed order)
 template <typename T>
 __device__ __forceinline__ void cgs_fold(const T* partial, int cnt, T* dst, bool do_sqrt) {
   if (blockIdx.x != 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int j = warp; j < cnt; j += kCgsThreads / 32) {
+  for (int j = warp; j < cnt; j += kCgsWarps) {
     T a = T(0);
     for (int b = lane; b < (int)gridDim.x; b += 32) a += __ldcg(partial + (int64_t)j * gridDim.x + b);
 #pragma unroll
@@ -111,126 +96,196 @@ __device__ __forceinline__ void cgs_fold(const T* partial, int cnt, T* dst, bool
   }
 }
 
-// MODE 0: acc[j] += q_j w            (pass A)
-// MODE 1: w -= sum q_j h; acc[j] += q_j w   (pass B)
-// MODE 2: w -= sum q_j h; acc[0] += w^2     (pass C)
-template <typename T, int KB, int MODE>
-__device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const CUtensorMap* qmap, T* sq, T* sw, T* sh,
-                                         uint64_t* bars, uint32_t& phases, const T* h, T (&acc)[KB]) {
-  const int64_t ntiles = (p.n + p.tile - 1) / p.tile;
+// Warp roles: WR warps split the rows (row group rg = warp % WR streams rows
+// rg, rg+WR, ...), WE = W/WR element groups split the tiles, so small bases
+// still keep every warp streaming.
+// MODE 0: acc[r] += q_{j(r)} . w                       (pass A)
+// MODE 1: w -= sum_j q_j h_j ; acc[r] += q_{j(r)} . w   (pass B)
+// MODE 2: w -= sum_j q_j h_j ; acc[0] += w . w (rg 0)   (pass C)
+template <typename T, int WR, int RPW, int U, int MODE>
+__device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const T* h, T (&acc)[RPW],
+                                         typename Vec16<T>::V* red) {
+  using V = typename Vec16<T>::V;
+  constexpr int VN = Vec16<T>::N;
+  constexpr int TILE = 32 * VN;  // elements per warp-wide 512 B load
+  constexpr int WE = kCgsWarps / WR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rg = warp % WR, eg = warp / WR;
+  const int kb = p.kb;
+  T hr[RPW];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    const int j = rg + r * WR;
+    hr[r] = (MODE > 0 && j < kb) ? __ldcg(h + j) : T(0);
+  }
+  // this CTA's contiguous range of tiles; element group eg takes U of every WE*U
+  const int64_t ntiles = (p.n + TILE - 1) / TILE;
   const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * per;
   const int64_t t1 = t0 + per < ntiles ? t0 + per : ntiles;
-  const int S = p.stages;
-  const int kb = p.kb;
-  if (MODE > 0 && threadIdx.x < kb) sh[threadIdx.x] = __ldcg(h + threadIdx.x);
-  __syncthreads();
-
-  auto issue = [&](int64_t t) {
-    const int st = (int)((t - t0) % S);
-    const int64_t i0 = t * p.tile;
-    const int64_t cnt = p.n - i0 < p.tile ? p.n - i0 : p.tile;
-    const uint32_t bytes = (uint32_t)(((cnt * sizeof(T)) + 15) & ~(int64_t)15);
-    T* qs = sq + (int64_t)st * kb * p.tile;
-    // tensor copies always land full boxes (zero-filled past n); stage layout [box b][row j][box]
-    const int nbx = (int)((cnt + p.box - 1) / p.box);
-    mbar_expect_tx(&bars[st], (uint32_t)(nbx * p.box * kb * sizeof(T)) + bytes);
-    for (int b = 0; b < nbx; ++b)
-      tma_2d_g2s(qs + (int64_t)b * kb * p.box, qmap, (int)(i0 + (int64_t)b * p.box), 0, &bars[st]);
-    bulk_g2s(sw + (int64_t)st * p.tile, p.w + i0, bytes, &bars[st]);
-  };
-
-  if (threadIdx.x == 0)
-    for (int64_t t = t0; t < t1 && t < t0 + S - 1; ++t) issue(t);
-  for (int64_t t = t0; t < t1; ++t) {
-    if (threadIdx.x == 0 && t + S - 1 < t1) issue(t + S - 1);
-    const int st = (int)((t - t0) % S);
-    mbar_wait(&bars[st], (phases >> st) & 1u);
-    phases ^= 1u << st;
-    const T* qs = sq + (int64_t)st * kb * p.tile;
-    const T* ws = sw + (int64_t)st * p.tile;
-    const int64_t i0 = t * p.tile;
-    const int cnt = (int)(p.n - i0 < p.tile ? p.n - i0 : p.tile);
-    for (int e = threadIdx.x; e < cnt; e += kCgsThreads) {
-      const T* qe = qs + (int64_t)(e / p.box) * kb * p.box + (e % p.box);  // row j at qe[j * box]
-      T wi = ws[e];
-      if (MODE > 0) {
-        T ts = T(0);
+  for (int64_t tb = t0; tb < t1; tb += WE * U) {
+    V q[U][RPW];
+    V wv[U];
+    if (tb + WE * U <= t1 && (tb + WE * U) * TILE <= p.n) {  // full iteration: unpredicated loads
 #pragma unroll
-        for (int j = 0; j < KB; ++j)
-          if (j < kb) ts = fma(qe[j * p.box], sh[j], ts);
-        wi = wi - ts;
-        p.w[i0 + e] = wi;  // read back by the next pass's bulk copies (async proxy)
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = (tb + eg * U + u) * TILE + lane * VN;
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+          const int j = rg + r * WR;
+          q[u][r] = __ldcs((const V*)(p.Q + (j < kb ? j : 0) * p.ldq + i));
+          if (j >= kb) q[u][r] = V{};
+        }
+        wv[u] = __ldcg((const V*)(p.w + i));
       }
-      if (MODE < 2) {
+    } else {
 #pragma unroll
-        for (int j = 0; j < KB; ++j)
-          if (j < kb) acc[j] = fma(qe[j * p.box], wi, acc[j]);
-      } else {
-        acc[0] = fma(wi, wi, acc[0]);
+      for (int u = 0; u < U; ++u) {
+        const int64_t tile = tb + eg * U + u;
+        const int64_t i = tile * TILE + lane * VN;
+        const bool in = tile < t1 && i < p.n;
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+          const int j = rg + r * WR;
+          q[u][r] = (in && j < kb) ? __ldcs((const V*)(p.Q + j * p.ldq + i)) : V{};
+        }
+        wv[u] = in ? __ldcg((const V*)(p.w + i)) : V{};
       }
     }
-    __syncthreads();  // stage st free for refill
+    if (MODE > 0) {
+      if (WR > 1) {
+        // this warp's share of the correction, then the sum over the row group (fixed order)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          V t{};
+#pragma unroll
+          for (int c = 0; c < VN; ++c) {
+            T s = T(0);
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) s = fma(vget<T>(q[u][r], c), hr[r], s);
+            vset<T>(t, c, s);
+          }
+          red[(u * kCgsWarps + warp) * 32 + lane] = t;
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        V tot;
+        if (WR > 1) {
+          tot = red[(u * kCgsWarps + eg * WR) * 32 + lane];
+          for (int v = 1; v < WR; ++v) {
+            const V x = red[(u * kCgsWarps + eg * WR + v) * 32 + lane];
+#pragma unroll
+            for (int c = 0; c < VN; ++c) vset<T>(tot, c, vget<T>(tot, c) + vget<T>(x, c));
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < VN; ++c) {
+            T s = T(0);
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) s = fma(vget<T>(q[u][r], c), hr[r], s);
+            vset<T>(tot, c, s);
+          }
+        }
+        V nw;
+#pragma unroll
+        for (int c = 0; c < VN; ++c) vset<T>(nw, c, vget<T>(wv[u], c) - vget<T>(tot, c));
+        wv[u] = nw;
+        const int64_t tile = tb + eg * U + u;
+        const int64_t i = tile * TILE + lane * VN;
+        if (rg == 0 && tile < t1 && i < p.n) *(V*)(p.w + i) = nw;
+      }
+      if (WR > 1) __syncthreads();  // partials consumed before the next iteration overwrites them
+    }
+    if (MODE < 2) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < RPW; ++r)
+#pragma unroll
+          for (int c = 0; c < VN; ++c) acc[r] = fma(vget<T>(q[u][r], c), vget<T>(wv[u], c), acc[r]);
+    } else if (rg == 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int c = 0; c < VN; ++c) acc[0] = fma(vget<T>(wv[u], c), vget<T>(wv[u], c), acc[0]);
+    }
   }
 }
 
-template <typename T, int KB>
-__global__ void __launch_bounds__(kCgsThreads, 1) k_cgs2_fused(const __grid_constant__ CgsParams<T> p,
-                                                              const __grid_constant__ CUtensorMap qmap) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* sq = (T*)smem_raw;                                   // [S][kb][tile]
-  T* sw = sq + (int64_t)p.stages * p.kb * p.tile;         // [S][tile]
-  T* red = sw + (int64_t)p.stages * p.tile;               // [warps][KB]
-  T* sh = red + (kCgsThreads / 32) * KB;                  // [KB] current h
-  uint64_t* bars = (uint64_t*)(sh + KB + 2);
-  bars = (uint64_t*)(((uintptr_t)bars + 7) & ~(uintptr_t)7);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < p.stages; ++s) mbar_init(&bars[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+// rows -> partial[j][block]: lane reduce per warp, then element groups added in order
+template <typename T, int WR, int RPW>
+__device__ __forceinline__ void cgs_store_rows(const T (&acc)[RPW], int kb, T* partial, T* sacc) {
+  constexpr int WE = kCgsWarps / WR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    T a = acc[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) sacc[warp * RPW + r] = a;
   }
   __syncthreads();
-  uint32_t phases = 0;
+  if (threadIdx.x < kb) {
+    const int j = threadIdx.x, rg = j % WR, r = j / WR;
+    T a = sacc[rg * RPW + r];
+    for (int e = 1; e < WE; ++e) a += sacc[(e * WR + rg) * RPW + r];
+    partial[(int64_t)j * gridDim.x + blockIdx.x] = a;
+  }
+  __syncthreads();
+}
 
+template <typename T, int WR, int RPW, int U>
+__global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_constant__ CgsParams<T> p) {
+  namespace cg = cooperative_groups;
+  using V = typename Vec16<T>::V;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ V red[WR > 1 ? U * kCgsWarps * 32 : 1];
+  __shared__ T sacc[kCgsWarps * RPW];
   {  // pass A: h1
-    T acc[KB];
+    T acc[RPW];
 #pragma unroll
-    for (int j = 0; j < KB; ++j) acc[j] = T(0);
-    cgs_pass<T, KB, 0>(p, &qmap, sq, sw, sh, bars, phases, nullptr, acc);
-    cgs_block_reduce<T, KB>(acc, p.kb, p.partial, red);
+    for (int r = 0; r < RPW; ++r) acc[r] = T(0);
+    cgs_pass<T, WR, RPW, U, 0>(p, nullptr, acc, red);
+    cgs_store_rows<T, WR, RPW>(acc, p.kb, p.partial, sacc);
   }
   grid.sync();
   cgs_fold(p.partial, p.kb, p.scal, false);
   grid.sync();
   {  // pass B: w -= Q^T h1 ; h2
-    T acc[KB];
+    T acc[RPW];
 #pragma unroll
-    for (int j = 0; j < KB; ++j) acc[j] = T(0);
-    cgs_pass<T, KB, 1>(p, &qmap, sq, sw, sh, bars, phases, p.scal, acc);
-    cgs_block_reduce<T, KB>(acc, p.kb, p.partial, red);
+    for (int r = 0; r < RPW; ++r) acc[r] = T(0);
+    cgs_pass<T, WR, RPW, U, 1>(p, p.scal, acc, red);
+    cgs_store_rows<T, WR, RPW>(acc, p.kb, p.partial, sacc);
   }
-  asm volatile("fence.proxy.async;" ::: "memory");  // generic w stores -> async-proxy reads
   grid.sync();
   cgs_fold(p.partial, p.kb, p.scal + 64, false);
   grid.sync();
-  {  // pass C: w -= Q^T h2 ; beta^2
-    T acc[KB];
+  {  // pass C: w -= Q^T h2 ; beta^2 (row-group-0 warps hold the block's share)
+    T acc[RPW];
 #pragma unroll
-    for (int j = 0; j < KB; ++j) acc[j] = T(0);
-    cgs_pass<T, KB, 2>(p, &qmap, sq, sw, sh, bars, phases, p.scal + 64, acc);
-    T a1[1] = {acc[0]};
-    cgs_block_reduce<T, 1>(a1, 1, p.partial, red);
+    for (int r = 0; r < RPW; ++r) acc[r] = T(0);
+    cgs_pass<T, WR, RPW, U, 2>(p, p.scal + 64, acc, red);
+    cgs_store_rows<T, WR, RPW>(acc, 1, p.partial, sacc);
   }
-  asm volatile("fence.proxy.async;" ::: "memory");
   if (p.qnext == nullptr) return;
   grid.sync();
   cgs_fold(p.partial, 1, p.scal + 128, true);
   grid.sync();
-  // pass D: Q[k+1] = w / beta  (ref: krylov.py:269-273)
+  // pass D: Q[k+1] = w / beta  (ref: krylov.py:269-273), 16-byte vectors
+  using VV = typename Vec16<T>::V;
+  constexpr int VN = Vec16<T>::N;
   const T bt = __ldcg(p.scal + 128);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x)
-    p.qnext[i] = bt != T(0) ? div_rn(__ldcg(p.w + i), bt) : T(0);
+  const int64_t nv = p.n / VN;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const VV x = __ldcg((const VV*)p.w + v);
+    VV y;
+#pragma unroll
+    for (int c = 0; c < VN; ++c) vset<T>(y, c, bt != T(0) ? div_rn(vget<T>(x, c), bt) : T(0));
+    ((VV*)p.qnext)[v] = y;
+  }
 }
 
 }  // namespace hpg

@@ -207,13 +207,14 @@ def test_large_grid_properties():
 
 
 @pytest.mark.parametrize("dt", ["f32", "f64"])
-def test_fused_cgs2_matches_per_pass_kernels(dt):
+@pytest.mark.parametrize("L", [4, 6, 32, 40])
+def test_fused_cgs2_matches_per_pass_kernels(dt, L):
     """The cooperative bulk-copy CGS2 and the per-pass kernels orthogonalise alike
     (same arithmetic per element, reductions differ only in grouping)."""
     import ctypes as C
     from paper_2507_11512_b200 import _lib
     from paper_2507_11512_b200.krylov import GmresWorkspace
-    h = _hier(32, 2)
+    h = _hier(L, 1)
     ctx = h.ctx
     n = h.levels[0].A_hi.n_rows
     npdt = np.float32 if dt == "f32" else np.float64
