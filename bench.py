@@ -221,9 +221,11 @@ def run_ours(args):
     ddev_s, dwall_s, diters, _, _ = timed("double", args.steps)
 
     # e2e through the public API with host buffers (H2D b, D2H x inside the region)
-    b_host = b.cpu().numpy()
-    x_host = np.zeros(n)
-    b_pin = torch.from_numpy(b_host).pin_memory().numpy()
+    # pinned host buffers (the public API accepts numpy arrays; pinned ones DMA directly)
+    b_pin = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    b_pin.copy_(b)
+    b_pin = b_pin.numpy()
+    x_host = torch.zeros(n, dtype=torch.float64, pin_memory=True).numpy()
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):

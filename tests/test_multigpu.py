@@ -1,0 +1,61 @@
+"""Multi-GPU parity (2 GPUs or more): bitwise kernels vs the oracle's all-rank
+simulation and solver counts vs the reference (tests/golden/solves.json r2l16:
+23 double, mixed envelope), through torchrun + NCCL.  Skips on 1-GPU boxes."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def _run(nproc, L, levels):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--local-addr", "127.0.0.1",
+           "--nproc-per-node", str(nproc), os.path.join(ROOT, "tools", "mgpu_check.py"), str(L), str(levels)]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    line = [x for x in p.stdout.splitlines() if x.startswith("{")][-1]
+    return json.loads(line)
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs 2 GPUs")
+def test_two_ranks_16():
+    out = _run(2, 16, 4)
+    for rk in out["checks"]:
+        assert all(rk.values()), out["checks"]
+    ref = load_golden("solves.json")["r2l16"]
+    assert out["solves"]["double"]["iterations"] == ref["1"]["double"]["iterations"] == 23
+    env = [ref[t]["mixed"]["iterations"] for t in ("1", "default")]
+    ncyc = len(ref["1"]["mixed"]["cycle_iters"])
+    assert min(env) - ncyc <= out["solves"]["mixed"]["iterations"] <= max(env) + ncyc
+    assert out["solves"]["mixed"]["relres"] < 1e-9
+
+
+@pytest.mark.skipif(_gpus() < 4, reason="needs 4 GPUs")
+def test_four_ranks_8():
+    out = _run(4, 8, 4)
+    for rk in out["checks"]:
+        assert all(rk.values()), out["checks"]
+    assert out["solves"]["double"]["converged"] and out["solves"]["mixed"]["relres"] < 1e-9
+
+
+@pytest.mark.skipif(_gpus() < 8, reason="needs 8 GPUs")
+def test_eight_ranks_8():
+    # ref: tests/test_acceptance.py:347-348 -> 8 ranks x 8^3: 18 double / 23 mixed
+    out = _run(8, 8, 4)
+    for rk in out["checks"]:
+        assert all(rk.values()), out["checks"]
+    assert out["solves"]["double"]["iterations"] == 18
+    assert abs(out["solves"]["mixed"]["iterations"] - 23) <= 2
