@@ -133,7 +133,8 @@ int64_t hpg_launch_count(hpg_ctx* ctx);
 int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
 /* Tuning switches (results are identical up to reduction order):
  *   "cgs_fused"  1: single-rank CGS2 as one cooperative bulk-copy kernel, 0: per-pass kernels
- *   "tail_rows"  levels with at most this many rows run in the persistent V-cycle tail kernel */
+ *   "tail_rows"  levels with at most this many rows run in the persistent V-cycle tail kernel
+ *   "pdl"        1: stencil kernels use programmatic dependent launch */
 int hpg_set_option(hpg_ctx* ctx, const char* key, int64_t value);
 
 #ifdef __cplusplus

@@ -174,11 +174,12 @@ struct hpg_ctx {
   void* partial = nullptr;      // nb * 64 elements (f64-sized)
   double* spmv_partial = nullptr;
   int64_t spmv_partial_len = 0;
-  void* scal = nullptr;         // 256 f64-sized device scalars
+  void* scal = nullptr;         // 512 f64-sized device scalars
   void* gather = nullptr;       // nranks * 256
   double* pinned = nullptr;     // 256 host doubles
   int64_t launches = 0;
   bool cgs_fused = true;
+  bool pdl = true;
   int64_t tail_rows = 0;        // levels with n <= tail_rows run in the persistent tail kernel
   int tail_blocks[2] = {0, 0};  // cooperative grid (f64, f32)
   // per-motif CUDA-event timers (ref: metrics.py:125-131 Tally.timed)
@@ -224,6 +225,24 @@ float* vals_of<float>(const Level& L) { return L.v32; }
 
 int grid_for(int64_t n, int threads = 256) { return (int)std::max<int64_t>(1, cdiv(n, threads)); }
 
+// Launch with programmatic dependent launch (PDL) enabled: the kernel may begin
+// while its stream predecessor drains (kernels call griddepcontrol.wait before
+// touching predecessor-produced data; see hpg_kernels.cuh pdl_wait).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(hpg_ctx* c, void (*k)(KArgs...), int grid, int block, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = c->pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...);
+}
+
 int do_exchange(hpg_ctx* c, int l, int prec, void* v) {
   Level& L = c->lev[l];
   if (c->nranks == 1 || L.nbrs.empty()) return HPG_OK;
@@ -263,7 +282,8 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
   Timed tm(c, M_GS);
   Level& L = c->lev[l];
   if (zero) {
-    CUDA_TRY(cudaMemsetAsync(z, 0, L.n_ext * sizeof(T), c->stream));
+    CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n_ext, 4)), 256, z, L.n_ext));
+    ++c->launches;
   } else {
     int rc = do_exchange(c, l, sizeof(T) == 8 ? HPG_F64 : HPG_F32, z);
     if (rc) return rc;
@@ -272,8 +292,7 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
   for (int col = 0; col < L.g.ncolors; ++col) {
     const int64_t a = L.g.off[col], b = L.g.off[col + 1];
     if (b <= a) continue;
-    hpg::k_gs_pass<T><<<grid_for(b - a), 256, 0, c->stream>>>(L.cols, vals, L.ld, a, b - a, r, z);
-    LAUNCH_CHECK();
+    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T>, grid_for(b - a), 256, L.cols, vals, L.ld, a, b - a, r, z));
     ++c->launches;
   }
   return HPG_OK;
@@ -284,8 +303,8 @@ int restrict_(hpg_ctx* c, int l, const T* rf, const T* zf, T* rcoarse) {
   Timed tm(c, M_RESTRICT);
   Level& F = c->lev[l];
   Level& C = c->lev[l + 1];
-  hpg::k_restrict<T><<<grid_for(C.n), 256, 0, c->stream>>>(F.cols, vals_of<T>(F), F.ld, C.n, C.inj, rf, zf, rcoarse);
-  LAUNCH_CHECK();
+  CUDA_TRY(launch_pdl(c, hpg::k_restrict<T>, grid_for(C.n), 256, F.cols, (const T*)vals_of<T>(F), F.ld, C.n,
+                      (const int32_t*)C.inj, rf, zf, rcoarse));
   ++c->launches;
   return HPG_OK;
 }
@@ -294,8 +313,7 @@ template <typename T>
 int prolong_(hpg_ctx* c, int l, T* zf, const T* zc) {
   Timed tm(c, M_PROLONG);
   Level& C = c->lev[l + 1];
-  hpg::k_prolong<T><<<grid_for(C.n), 256, 0, c->stream>>>(C.n, C.inj, zf, zc);
-  LAUNCH_CHECK();
+  CUDA_TRY(launch_pdl(c, hpg::k_prolong<T>, grid_for(C.n), 256, C.n, (const int32_t*)C.inj, zf, zc));
   ++c->launches;
   return HPG_OK;
 }
@@ -476,42 +494,42 @@ int cgs2_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext, double* out) {
   return HPG_OK;
 }
 
-struct YArr {
-  double y[64];
-};
-
-template <typename T, int KB>
-__global__ void k_gemv_combine_y(const T* __restrict__ Q, int64_t ldq, int k, YArr y, T* __restrict__ out,
-                                 int64_t n) {
-  T yr[KB];
-#pragma unroll
-  for (int j = 0; j < KB; ++j) yr[j] = j < k ? (T)y.y[j] : T(0);
-  int64_t lo, hi;
-  hpg::block_chunk(n, lo, hi);
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    T a = T(0);
-#pragma unroll
-    for (int j = 0; j < KB; ++j)
-      if (j < k) a = fma(Q[j * ldq + i], yr[j], a);
-    out[i] = a;
-  }
-}
-
-template <typename T>
-int gemv_t(hpg_ctx* c, const T* Q, int64_t ldq, int k, const double* y, T* out) {
-  Timed tm(c, M_ORTHO);
-  YArr ya;
-  memset(&ya, 0, sizeof ya);
-  for (int j = 0; j < k; ++j) ya.y[j] = y[j];
-  const int64_t n = c->lev[0].n;
-  if (k <= 8) k_gemv_combine_y<T, 8><<<c->nb, 256, 0, c->stream>>>(Q, ldq, k, ya, out, n);
-  else if (k <= 16) k_gemv_combine_y<T, 16><<<c->nb, 256, 0, c->stream>>>(Q, ldq, k, ya, out, n);
-  else if (k <= 32) k_gemv_combine_y<T, 32><<<c->nb, 256, 0, c->stream>>>(Q, ldq, k, ya, out, n);
-  else if (k <= 64) k_gemv_combine_y<T, 64><<<c->nb, 256, 0, c->stream>>>(Q, ldq, k, ya, out, n);
-  else return fail(HPG_E_UNSUPPORTED, "restart length %d exceeds 64", k);
+template <typename T, int WR, int RPW, int U>
+int gemv_launch(hpg_ctx* c, const T* Q, int64_t ldq, int k, T* out) {
+  hpg::CgsParams<T> p;
+  memset(&p, 0, sizeof p);
+  p.Q = Q;
+  p.w = out;
+  p.scal = (T*)c->scal + 320;
+  p.ldq = ldq;
+  p.n = c->lev[0].n;
+  p.kb = k;
+  int per = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hpg::k_gemv_combine<T, WR, RPW, U>, hpg::kCgsThreads, 0));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  hpg::k_gemv_combine<T, WR, RPW, U><<<std::max(1, per) * sms, hpg::kCgsThreads, 0, c->stream>>>(p);
   LAUNCH_CHECK();
   ++c->launches;
   return HPG_OK;
+}
+
+// out = Q[0:k]^T y with y narrowed to T on the host first (ref: krylov.py:288-289)
+template <typename T>
+int gemv_t(hpg_ctx* c, const T* Q, int64_t ldq, int k, const double* y, T* out) {
+  Timed tm(c, M_ORTHO);
+  if (k > 64) return fail(HPG_E_UNSUPPORTED, "restart length %d exceeds 64", k);
+  if (ldq % 32 || c->lev[0].n % (16 / (int)sizeof(T))) return fail(HPG_E_ARG, "unaligned basis for gemv");
+  T yt[64];
+  for (int j = 0; j < k; ++j) yt[j] = (T)y[j];
+  CUDA_TRY(cudaMemcpyAsync((T*)c->scal + 320, yt, k * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  if (k <= 1) return gemv_launch<T, 1, 1, 8>(c, Q, ldq, k, out);
+  if (k <= 2) return gemv_launch<T, 2, 1, 8>(c, Q, ldq, k, out);
+  if (k <= 4) return gemv_launch<T, 4, 1, 8>(c, Q, ldq, k, out);
+  if (k <= 8) return gemv_launch<T, 4, 2, 4>(c, Q, ldq, k, out);
+  if (k <= 16) return gemv_launch<T, 8, 2, 4>(c, Q, ldq, k, out);
+  if (k <= 32) return gemv_launch<T, 8, 4, 2>(c, Q, ldq, k, out);
+  return gemv_launch<T, 8, 8, 1>(c, Q, ldq, k, out);
 }
 
 void free_level(Level& L) {
@@ -694,9 +712,11 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   {
     const char* e = getenv("HPG_TAIL_ROWS");
-    c->tail_rows = e ? atoll(e) : (int64_t)2200000;
+    c->tail_rows = e ? atoll(e) : (int64_t)0;  // measured: per-pass PDL kernels win at 256^3
     const char* f = getenv("HPG_CGS_FUSED");
     c->cgs_fused = !(f && f[0] == '0');
+    const char* g = getenv("HPG_PDL");
+    c->pdl = !(g && g[0] == '0');
     int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hpg::k_vcycle_tail<double>, 256, 0);
     c->tail_blocks[0] = std::max(1, per) * sms;
@@ -708,7 +728,7 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
   // partials: [64][grid] for the per-pass kernels (nb CTAs) and the cooperative ones (<= 8 per SM)
   if (dmalloc((char**)&c->partial, (size_t)std::max(c->nb, 8 * sms) * 64 * 8, nullptr) ||
       dmalloc(&c->spmv_partial, c->spmv_partial_len * 8, nullptr) ||
-      dmalloc((char**)&c->scal, 256 * 8, nullptr) || dmalloc((char**)&c->gather, (size_t)nranks * 256 * 8, nullptr))
+      dmalloc((char**)&c->scal, 512 * 8, nullptr) || dmalloc((char**)&c->gather, (size_t)nranks * 256 * 8, nullptr))
     return bail(HPG_E_CUDA);
   if (cudaMallocHost((void**)&c->pinned, 256 * 8) != cudaSuccess) return bail(fail(HPG_E_CUDA, "pinned alloc"));
   if (nranks > 1) {
@@ -806,12 +826,13 @@ int hpg_spmv(hpg_ctx* c, int l, int prec, void* x, void* y) {
   Level& L = c->lev[l];
   if (!L.n) return HPG_OK;
   if (prec == HPG_F64)
-    hpg::k_spmv<double, 0><<<grid_for(L.n), 256, 0, c->stream>>>(L.cols, L.v64, L.ld, 0, L.n, (const double*)x,
-                                                                  nullptr, (double*)y, nullptr);
+    CUDA_TRY(launch_pdl(c, hpg::k_spmv<double, 0>, grid_for(L.n), 256, (const int32_t*)L.cols,
+                        (const double*)L.v64, L.ld, (int64_t)0, L.n, (const double*)x, (const double*)nullptr,
+                        (double*)y, (double*)nullptr));
   else
-    hpg::k_spmv<float, 0><<<grid_for(L.n), 256, 0, c->stream>>>(L.cols, L.v32, L.ld, 0, L.n, (const float*)x,
-                                                                 nullptr, (float*)y, nullptr);
-  LAUNCH_CHECK();
+    CUDA_TRY(launch_pdl(c, hpg::k_spmv<float, 0>, grid_for(L.n), 256, (const int32_t*)L.cols, (const float*)L.v32,
+                        L.ld, (int64_t)0, L.n, (const float*)x, (const float*)nullptr, (float*)y,
+                        (double*)nullptr));
   ++c->launches;
   return HPG_OK;
 }
@@ -967,6 +988,7 @@ int64_t hpg_launch_count(hpg_ctx* c) { return c ? c->launches : -1; }
 int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(HPG_E_ARG, "null argument");
   if (!strcmp(key, "cgs_fused")) c->cgs_fused = value != 0;
+  else if (!strcmp(key, "pdl")) c->pdl = value != 0;
   else if (!strcmp(key, "tail_rows")) c->tail_rows = value;
   else return fail(HPG_E_ARG, "unknown option %s", key);
   return HPG_OK;

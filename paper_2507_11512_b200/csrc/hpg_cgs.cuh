@@ -102,6 +102,7 @@ __device__ __forceinline__ void cgs_fold(const T* partial, int cnt, T* dst, bool
 // MODE 0: acc[r] += q_{j(r)} . w                       (pass A)
 // MODE 1: w -= sum_j q_j h_j ; acc[r] += q_{j(r)} . w   (pass B)
 // MODE 2: w -= sum_j q_j h_j ; acc[0] += w . w (rg 0)   (pass C)
+// MODE 3: w  = sum_j q_j h_j                           (end-of-cycle basis combination)
 template <typename T, int WR, int RPW, int U, int MODE>
 __device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const T* h, T (&acc)[RPW],
                                          typename Vec16<T>::V* red) {
@@ -136,7 +137,7 @@ __device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const T* h, T (&
           q[u][r] = __ldcs((const V*)(p.Q + (j < kb ? j : 0) * p.ldq + i));
           if (j >= kb) q[u][r] = V{};
         }
-        wv[u] = __ldcg((const V*)(p.w + i));
+        if (MODE != 3) wv[u] = __ldcg((const V*)(p.w + i));
       }
     } else {
 #pragma unroll
@@ -149,7 +150,7 @@ __device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const T* h, T (&
           const int j = rg + r * WR;
           q[u][r] = (in && j < kb) ? __ldcs((const V*)(p.Q + j * p.ldq + i)) : V{};
         }
-        wv[u] = in ? __ldcg((const V*)(p.w + i)) : V{};
+        wv[u] = (in && MODE != 3) ? __ldcg((const V*)(p.w + i)) : V{};
       }
     }
     if (MODE > 0) {
@@ -189,8 +190,12 @@ __device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const T* h, T (&
           }
         }
         V nw;
+        if (MODE == 3) {
+          nw = tot;
+        } else {
 #pragma unroll
-        for (int c = 0; c < VN; ++c) vset<T>(nw, c, vget<T>(wv[u], c) - vget<T>(tot, c));
+          for (int c = 0; c < VN; ++c) vset<T>(nw, c, vget<T>(wv[u], c) - vget<T>(tot, c));
+        }
         wv[u] = nw;
         const int64_t tile = tb + eg * U + u;
         const int64_t i = tile * TILE + lane * VN;
@@ -205,7 +210,7 @@ __device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const T* h, T (&
         for (int r = 0; r < RPW; ++r)
 #pragma unroll
           for (int c = 0; c < VN; ++c) acc[r] = fma(vget<T>(q[u][r], c), vget<T>(wv[u], c), acc[r]);
-    } else if (rg == 0) {
+    } else if (MODE == 2 && rg == 0) {
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -286,6 +291,16 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
     for (int c = 0; c < VN; ++c) vset<T>(y, c, bt != T(0) ? div_rn(vget<T>(x, c), bt) : T(0));
     ((VV*)p.qnext)[v] = y;
   }
+}
+
+// out = Q[0:k]^T y (ref: krylov.py:288-289): one streaming pass over k rows,
+// same warp roles as CGS2; y (narrowed to T) sits in p.scal[0..k).
+template <typename T, int WR, int RPW, int U>
+__global__ void __launch_bounds__(kCgsThreads, 2) k_gemv_combine(const __grid_constant__ CgsParams<T> p) {
+  using V = typename Vec16<T>::V;
+  __shared__ V red[WR > 1 ? U * kCgsWarps * 32 : 1];
+  T acc[RPW];
+  cgs_pass<T, WR, RPW, U, 3>(p, p.scal, acc, red);
 }
 
 }  // namespace hpg

@@ -46,6 +46,13 @@ __device__ __forceinline__ double ld_stream(const double* p) {
   return v;
 }
 
+// Programmatic dependent launch: a kernel launched with the PDL attribute may
+// start while its predecessor drains; it issues its predecessor-independent
+// loads (the matrix planes) first and waits here before touching anything the
+// predecessor writes or reads.  Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------ stencil kernels
 //
 // Every stencil kernel handles one row per thread and is written "all loads
@@ -66,7 +73,7 @@ __device__ __forceinline__ T ldv(const T* p) {
   return *p;
 }
 
-template <typename T, bool ZERO_DIAG, bool COHERENT = false>
+template <typename T, bool ZERO_DIAG, bool COHERENT = false, bool PDL = false>
 __device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                             int64_t ld, int64_t i, const T* x, T* d) {
   int32_t c[27];
@@ -75,6 +82,7 @@ __device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, co
   for (int s = 0; s < 27; ++s) c[s] = ld_stream(cols + s * ld + i);
 #pragma unroll
   for (int s = 0; s < 27; ++s) v[s] = ld_stream(vals + s * ld + i);
+  if (PDL) pdl_wait();  // x may be written by the predecessor kernel
   T g[27];
 #pragma unroll
   for (int s = 0; s < 27; ++s) g[s] = ldv<COHERENT>(x + (c[s] < 0 ? ~c[s] : c[s]));
@@ -98,12 +106,13 @@ __global__ void __launch_bounds__(256, 2) k_spmv(const int32_t* __restrict__ col
                                                  int64_t ld, int64_t row0, int64_t nrows,
                                                  const T* __restrict__ x, const T* __restrict__ b,
                                                  T* __restrict__ y, double* __restrict__ partial) {
+  pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double sq = 0.0;
   if (t < nrows) {
     const int64_t i = row0 + t;
     T dd;
-    const T acc = row_accumulate<T, false>(cols, vals, ld, i, x, &dd);
+    const T acc = row_accumulate<T, false, false, MODE == 0>(cols, vals, ld, i, x, &dd);
     if (MODE == 0) {
       y[i] = acc;
     } else {
@@ -129,11 +138,11 @@ __global__ void __launch_bounds__(256, 2) k_spmv(const int32_t* __restrict__ col
 
 // One color pass of forward Gauss-Seidel over rows [row0, row0+nrows):
 //   z_i = (r_i - sum_{s != diag} A[i,s] z[col]) / a_ii
-template <typename T, bool COHERENT = false>
+template <typename T, bool COHERENT = false, bool PDL = false>
 __device__ __forceinline__ void gs_row(const int32_t* __restrict__ cols, const T* __restrict__ vals, int64_t ld,
                                        int64_t i, const T* __restrict__ r, T* z) {
   T d = T(0);
-  const T acc = row_accumulate<T, true, COHERENT>(cols, vals, ld, i, z, &d);
+  const T acc = row_accumulate<T, true, COHERENT, PDL>(cols, vals, ld, i, z, &d);
   z[i] = div_rn(sub_rn(ldv<COHERENT>(r + i), acc), d);
 }
 
@@ -141,19 +150,20 @@ template <typename T>
 __global__ void __launch_bounds__(256, 2) k_gs_pass(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                                     int64_t ld, int64_t row0, int64_t nrows,
                                                     const T* __restrict__ r, T* z) {
+  pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nrows) return;
-  gs_row<T>(cols, vals, ld, row0 + t, r, z);
+  gs_row<T, false, true>(cols, vals, ld, row0 + t, r, z);
 }
 
 // Fused residual + injection: for fine color-0 row j < nc,
 //   rc[dst[j]] = r[j] - (A z)[j]     (ref: multigrid.py:107-128)
-template <typename T, bool COHERENT = false>
+template <typename T, bool COHERENT = false, bool PDL = false>
 __device__ __forceinline__ void restrict_row(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                              int64_t ld, int64_t j, const int32_t* __restrict__ dst,
                                              const T* __restrict__ r, const T* z, T* __restrict__ rc) {
   T dd;
-  const T acc = row_accumulate<T, false, COHERENT>(cols, vals, ld, j, z, &dd);
+  const T acc = row_accumulate<T, false, COHERENT, PDL>(cols, vals, ld, j, z, &dd);
   rc[dst[j]] = sub_rn(ldv<COHERENT>(r + j), acc);
 }
 
@@ -162,18 +172,35 @@ __global__ void __launch_bounds__(256, 2) k_restrict(const int32_t* __restrict__
                                                      int64_t ld, int64_t nc, const int32_t* __restrict__ dst,
                                                      const T* __restrict__ r, const T* __restrict__ z,
                                                      T* __restrict__ rc) {
+  pdl_trigger();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nc) return;
-  restrict_row<T>(cols, vals, ld, j, dst, r, z, rc);
+  restrict_row<T, false, true>(cols, vals, ld, j, dst, r, z, rc);
 }
 
 // Injection transpose: z[j] += zc[dst[j]]  (ref: multigrid.py:131-137)
 template <typename T>
 __global__ void k_prolong(int64_t nc, const int32_t* __restrict__ dst, T* __restrict__ z,
                           const T* __restrict__ zc) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nc) return;
   z[j] = add_rn(z[j], zc[dst[j]]);
+}
+
+// z[0, n) = 0 (the smoother's zero initial guess, ref: smoother.py:95-96)
+template <typename T>
+__global__ void k_zero(T* __restrict__ z, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i + 4 <= n && ((uintptr_t)(z + i) & 15) == 0) {
+    if (sizeof(T) == 4) *(float4*)(z + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+    else { *(double2*)(z + i) = make_double2(0., 0.); *(double2*)(z + i + 2) = make_double2(0., 0.); }
+  } else {
+    for (int64_t k = i; k < i + 4 && k < n; ++k) z[k] = T(0);
+  }
 }
 
 // ---------------------------------------------------------- halo pack
