@@ -180,6 +180,7 @@ struct hpg_ctx {
   int64_t launches = 0;
   bool cgs_fused = true;
   bool pdl = true;
+  int gs_minb = 3;
   int64_t tail_rows = 0;        // levels with n <= tail_rows run in the persistent tail kernel
   int tail_blocks[2] = {0, 0};  // cooperative grid (f64, f32)
   // per-motif CUDA-event timers (ref: metrics.py:125-131 Tally.timed)
@@ -292,7 +293,12 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
   for (int col = 0; col < L.g.ncolors; ++col) {
     const int64_t a = L.g.off[col], b = L.g.off[col + 1];
     if (b <= a) continue;
-    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T>, grid_for(b - a), 256, L.cols, vals, L.ld, a, b - a, r, z));
+    if (c->gs_minb == 3)
+      CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3>, grid_for(b - a), 256, L.cols, vals, L.ld, a, b - a, r, z));
+    else if (c->gs_minb == 4)
+      CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 4>, grid_for(b - a), 256, L.cols, vals, L.ld, a, b - a, r, z));
+    else
+      CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 2>, grid_for(b - a), 256, L.cols, vals, L.ld, a, b - a, r, z));
     ++c->launches;
   }
   return HPG_OK;
@@ -444,8 +450,76 @@ int cgs2_fused(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   return HPG_OK;
 }
 
+// multi-rank CGS2: the same streaming passes, one launch each, with the
+// rank-ordered all-reduce (NCCL all-gather + ordered fold) between them
+template <typename T, int WR, int RPW, int U>
+int cgs2_passes(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
+  hpg::CgsParams<T> p;
+  memset(&p, 0, sizeof p);
+  p.Q = Q;
+  p.w = w;
+  p.qnext = qnext;
+  p.partial = (T*)c->partial;
+  p.scal = (T*)c->scal;
+  p.ldq = ldq;
+  p.n = c->lev[0].n;
+  p.kb = kb;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int grid = 2 * sms;
+  T* scal = (T*)c->scal;
+  int rc;
+  hpg::k_cgs_onepass<T, WR, RPW, U, 0><<<grid, hpg::kCgsThreads, 0, c->stream>>>(p, (const T*)nullptr);
+  hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(p.partial, grid, kb, scal, 0);
+  LAUNCH_CHECK();
+  c->launches += 2;
+  if ((rc = allreduce_scal<T>(c, scal, kb))) return rc;
+  hpg::k_cgs_onepass<T, WR, RPW, U, 1><<<grid, hpg::kCgsThreads, 0, c->stream>>>(p, (const T*)scal);
+  hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(p.partial, grid, kb, scal + 64, 0);
+  LAUNCH_CHECK();
+  c->launches += 2;
+  if ((rc = allreduce_scal<T>(c, scal + 64, kb))) return rc;
+  hpg::k_cgs_onepass<T, WR, RPW, U, 2><<<grid, hpg::kCgsThreads, 0, c->stream>>>(p, (const T*)(scal + 64));
+  LAUNCH_CHECK();
+  c->launches += 1;
+  if (qnext) {
+    hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(p.partial, grid, 1, scal + 128, 0);
+    LAUNCH_CHECK();
+    if ((rc = allreduce_scal<T>(c, scal + 128, 1))) return rc;
+    hpg::k_sqrt_inplace<T><<<1, 1, 0, c->stream>>>(scal + 128);
+    hpg::k_scale<T><<<grid_for(p.n), 256, 0, c->stream>>>(w, scal + 128, qnext, p.n);
+    LAUNCH_CHECK();
+    c->launches += 3;
+  }
+  return HPG_OK;
+}
+
 template <typename T>
 int cgs2_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext, double* out) {
+  if (c->nranks > 1 && c->cgs_fused && c->lev[0].n % (16 / (int)sizeof(T)) == 0 && ldq % 32 == 0 && k + 1 <= 64) {
+    const int kb = k + 1;
+    int rc;
+    {
+      Timed tm(c, M_ORTHO);
+      if (kb <= 1) rc = cgs2_passes<T, 1, 1, 8>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 2) rc = cgs2_passes<T, 2, 1, 8>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 4) rc = cgs2_passes<T, 4, 1, 8>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 8) rc = cgs2_passes<T, 4, 2, 4>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 16) rc = cgs2_passes<T, 8, 2, 4>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 32) rc = cgs2_passes<T, 8, 4, 2>(c, Q, ldq, kb, w, qnext);
+      else rc = cgs2_passes<T, 8, 8, 1>(c, Q, ldq, kb, w, qnext);
+      if (rc) return rc;
+    }
+    CUDA_TRY(cudaMemcpyAsync(c->pinned, c->scal, 129 * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const T* hv = (const T*)c->pinned;
+    for (int j = 0; j < kb; ++j) {
+      out[j] = (double)hv[j];
+      out[kb + j] = (double)hv[64 + j];
+    }
+    out[2 * kb] = qnext ? (double)hv[128] : 0.0;
+    return HPG_OK;
+  }
   if (c->nranks == 1 && c->cgs_fused && c->lev[0].n % (16 / (int)sizeof(T)) == 0) {
     const int kb = k + 1;
     int rc;
@@ -715,6 +789,8 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     c->tail_rows = e ? atoll(e) : (int64_t)0;  // measured: per-pass PDL kernels win at 256^3
     const char* f = getenv("HPG_CGS_FUSED");
     c->cgs_fused = !(f && f[0] == '0');
+    const char* mb = getenv("HPG_GS_MINB");
+    if (mb) c->gs_minb = atoi(mb);
     const char* g = getenv("HPG_PDL");
     c->pdl = !(g && g[0] == '0');
     int per = 0;
@@ -989,6 +1065,7 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(HPG_E_ARG, "null argument");
   if (!strcmp(key, "cgs_fused")) c->cgs_fused = value != 0;
   else if (!strcmp(key, "pdl")) c->pdl = value != 0;
+  else if (!strcmp(key, "gs_minb")) c->gs_minb = (int)value;
   else if (!strcmp(key, "tail_rows")) c->tail_rows = value;
   else return fail(HPG_E_ARG, "unknown option %s", key);
   return HPG_OK;

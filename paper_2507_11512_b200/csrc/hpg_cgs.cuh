@@ -293,6 +293,22 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
   }
 }
 
+// One CGS2 pass per launch (multi-rank path: the cross-rank reduction of the
+// per-CTA partials -- NCCL all-gather + rank-ordered fold -- runs between the
+// passes).  MODE 0/1 write per-CTA row partials, MODE 2 the per-CTA norm share.
+template <typename T, int WR, int RPW, int U, int MODE>
+__global__ void __launch_bounds__(kCgsThreads, 2) k_cgs_onepass(const __grid_constant__ CgsParams<T> p,
+                                                               const T* __restrict__ h) {
+  using V = typename Vec16<T>::V;
+  __shared__ V red[WR > 1 ? U * kCgsWarps * 32 : 1];
+  __shared__ T sacc[kCgsWarps * RPW];
+  T acc[RPW];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) acc[r] = T(0);
+  cgs_pass<T, WR, RPW, U, MODE>(p, h, acc, red);
+  cgs_store_rows<T, WR, RPW>(acc, MODE == 2 ? 1 : p.kb, p.partial, sacc);
+}
+
 // out = Q[0:k]^T y (ref: krylov.py:288-289): one streaming pass over k rows,
 // same warp roles as CGS2; y (narrowed to T) sits in p.scal[0..k).
 template <typename T, int WR, int RPW, int U>

@@ -146,8 +146,8 @@ __device__ __forceinline__ void gs_row(const int32_t* __restrict__ cols, const T
   z[i] = div_rn(sub_rn(ldv<COHERENT>(r + i), acc), d);
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256, 2) k_gs_pass(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+template <typename T, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_gs_pass(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                                     int64_t ld, int64_t row0, int64_t nrows,
                                                     const T* __restrict__ r, T* z) {
   pdl_trigger();
