@@ -128,8 +128,9 @@ int hpg_allreduce_host(hpg_ctx* ctx, double* vals, int n);
 /* Number of kernels this context has launched (for the bench's gpu_launches). */
 int64_t hpg_launch_count(hpg_ctx* ctx);
 /* Per-motif CUDA-event timers (ref: metrics.py:111-143 Tally).  mode 1 enable,
- * 0 disable, 2 synchronise + ADD seconds per motif into seconds[6]
- * (GS, SpMV, Ortho, Restriction, Prolongation, Vector ops) and reset.      */
+ * 0 disable, 2 synchronise + ADD seconds per motif into seconds[8]
+ * (GS, SpMV, Ortho, Restriction, Prolongation, Vector ops, GS level-0 subset,
+ * reserved) and reset.                                                      */
 int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
 /* Tuning switches (results are identical up to reduction order):
  *   "cgs_fused"  1: single-rank CGS2 as one cooperative bulk-copy kernel, 0: per-pass kernels

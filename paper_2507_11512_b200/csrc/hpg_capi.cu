@@ -192,7 +192,7 @@ struct hpg_ctx {
 
 namespace {
 
-enum Motif { M_GS = 0, M_SPMV = 1, M_ORTHO = 2, M_RESTRICT = 3, M_PROLONG = 4, M_VEC = 5 };
+enum Motif { M_GS = 0, M_SPMV = 1, M_ORTHO = 2, M_RESTRICT = 3, M_PROLONG = 4, M_VEC = 5, M_GS_L0 = 6 };
 
 // RAII motif region: records an event pair on the compute stream when timing is on
 struct Timed {
@@ -200,7 +200,7 @@ struct Timed {
   int motif;
   size_t idx = (size_t)-1;
   Timed(hpg_ctx* c_, int m) : c(c_), motif(m) {
-    if (!c->timing) return;
+    if (!c->timing || m < 0) return;
     while (c->events.size() < c->ev_used + 2) {
       cudaEvent_t e;
       if (cudaEventCreate(&e) != cudaSuccess) return;
@@ -281,6 +281,7 @@ int allreduce_scal(hpg_ctx* c, T* buf, int cnt) {
 template <typename T>
 int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
   Timed tm(c, M_GS);
+  Timed tm0(c, l == 0 ? M_GS_L0 : -1);  // level-0 sweeps also timed alone (bench roofline)
   Level& L = c->lev[l];
   if (zero) {
     CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n_ext, 4)), 256, z, L.n_ext));
@@ -1072,7 +1073,8 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
 }
 
 // mode 1: enable, 0: disable, 2: synchronise, add each motif's seconds into
-// seconds[6] (GS, SpMV, Ortho, Restriction, Prolongation, Vector ops) and reset.
+// seconds[8] (GS, SpMV, Ortho, Restriction, Prolongation, Vector ops, GS at level 0
+// (a subset of GS), reserved) and reset.
 int hpg_timers(hpg_ctx* c, int mode, double* seconds) {
   if (!c) return fail(HPG_E_ARG, "null context");
   if (mode == 0 || mode == 1) {

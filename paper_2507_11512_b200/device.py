@@ -49,7 +49,7 @@ class Context:
         return int(_lib.lib().hpg_launch_count(self.h))
 
     def timers(self, mode, seconds=None):
-        out = np.zeros(6) if seconds is None else seconds
+        out = np.zeros(8) if seconds is None else seconds
         self.call("hpg_timers", mode, out.ctypes.data_as(C.POINTER(C.c_double)))
         return out
 

@@ -95,6 +95,9 @@ class Tally:
         self.flops = {m: 0 for m in MOTIFS}
         self.bytes = {m: 0 for m in MOTIFS}
         self.seconds = {m: 0.0 for m in MOTIFS}
+        self.gs_level0_seconds = 0.0   # additive: level-0 sweeps alone (subset of GS)
+        self.gs_level0_bytes = 0
+        self.gs_level0_sweeps = 0
 
     def add(self, kernel, dtype, motif=None, **sizes):
         bucket = motif or kernel_motif(kernel)
@@ -115,6 +118,7 @@ class Tally:
         sec = ctx.timers(2)
         for m, s in zip(MOTIFS, sec):
             self.seconds[m] += float(s)
+        self.gs_level0_seconds += float(sec[6])
 
     def total_flops(self):
         return sum(self.flops.values())
@@ -127,6 +131,9 @@ class Tally:
             self.flops[m] = 0
             self.bytes[m] = 0
             self.seconds[m] = 0.0
+        self.gs_level0_seconds = 0.0
+        self.gs_level0_bytes = 0
+        self.gs_level0_sweeps = 0
 
 
 def sum_motif_dicts(dicts):

@@ -86,6 +86,11 @@ def count_vcycle(h, tally, dtype):
         sweeps = sw.nu_c if last else sw.nu1 + sw.nu2
         for _ in range(sweeps):
             tally.add("gs_sweep", dtype, nnz=A.nnz_total, n=A.n_rows)
+            if lev == 0 and hasattr(tally, "gs_level0_bytes"):
+                from .metrics import count_bytes
+                tally.gs_level0_bytes += count_bytes("gs_sweep", np.dtype(dtype).itemsize,
+                                                     nnz=A.nnz_total, n=A.n_rows)
+                tally.gs_level0_sweeps += 1
         if not last:
             nxt = h.levels[lev + 1]
             tally.add("restrict_fused", dtype, nnz=nxt.inject_nnz, n_c=nxt.A_hi.n_rows)
