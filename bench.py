@@ -158,7 +158,7 @@ def run_ours(args):
     world = World(nproc) if nproc > 1 else None
     L = args.local
     cfg = BenchConfig(local_nx=L, local_ny=L, local_nz=L, ranks=nproc, time_seconds=0,
-                      max_iters=args.max_iters)
+                      max_iters=args.max_iters, validation_mode=args.validation)
     peak, peak_kind = _peaks()
 
     # validation (n_d, n_ir -> penalty), standard mode on one rank at the local size
@@ -324,6 +324,8 @@ def main():
     p.add_argument("--local", type=int, default=256)
     p.add_argument("--max-iters", type=int, default=300)
     p.add_argument("--no-validation", action="store_true")
+    p.add_argument("--validation", choices=("standard", "fullscale"), default="standard",
+                   help="standard: 1-rank solve at the local size; fullscale: all ranks, full problem")
     p.add_argument("--no-cpu", action="store_true")
     args = p.parse_args()
     if args.impl == "reference":
