@@ -115,14 +115,14 @@ class World:
         return acc
 
     def nccl_uid(self):
-        """One NCCL unique id for the job (rank 0 creates, everyone receives)."""
-        if self._uid is None:
-            from . import _lib
-            import ctypes as C
-            buf = (C.c_char * 128)()
-            if self.rank == 0:
-                _lib.check(_lib.lib().hpg_nccl_unique_id(buf, 128))
-            self._uid = self.broadcast_bytes(bytes(buf))
+        """A fresh NCCL unique id for a new communicator (collective: rank 0 creates,
+        every rank receives).  Each communicator needs its own id."""
+        from . import _lib
+        import ctypes as C
+        buf = (C.c_char * 128)()
+        if self.rank == 0:
+            _lib.check(_lib.lib().hpg_nccl_unique_id(buf, 128))
+        self._uid = self.broadcast_bytes(bytes(buf))
         return self._uid
 
     def run(self, fn, *args, **kwargs):

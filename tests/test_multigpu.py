@@ -41,6 +41,10 @@ def test_two_ranks_16():
     ncyc = len(ref["1"]["mixed"]["cycle_iters"])
     assert min(env) - ncyc <= out["solves"]["mixed"]["iterations"] <= max(env) + ncyc
     assert out["solves"]["mixed"]["relres"] < 1e-9
+    # fullscale validation over both ranks: same problem, same counts (ref bench.py:168-173)
+    assert out["validation"]["mode"] == "fullscale" and out["validation"]["n_d"] == 23
+    assert min(env) - ncyc <= out["validation"]["n_ir"] <= max(env) + ncyc
+    assert out["summary"]["raw_gflops"] > 0
 
 
 @pytest.mark.skipif(_gpus() < 4, reason="needs 4 GPUs")

@@ -72,9 +72,15 @@ def main():
                      "cycles": r.cycle_iterations,
                      "x_err": float((x0 - 1.0).abs().max().item())}
     h.close()
+    # the reference's full pipeline on the same world: fullscale validation (all
+    # ranks) + timed phases; builds two more hierarchies (fresh NCCL communicators)
+    from paper_2507_11512_b200.bench import BenchConfig, run_benchmark
+    rep = run_benchmark(BenchConfig(local_nx=L, local_ny=L, local_nz=L, ranks=R, time_seconds=0,
+                                    mg_levels=levels, validation_mode="fullscale"))
     allok = world.gather(rank, ok)
     if rank == 0:
-        print(json.dumps({"ranks": R, "local": L, "checks": allok, "solves": res}))
+        print(json.dumps({"ranks": R, "local": L, "checks": allok, "solves": res,
+                          "validation": rep["validation"], "summary": rep["summary"]}))
 
 
 if __name__ == "__main__":
