@@ -135,7 +135,9 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
 /* Tuning switches (results are identical up to reduction order):
  *   "cgs_fused"  1: single-rank CGS2 as one cooperative bulk-copy kernel, 0: per-pass kernels
  *   "tail_rows"  levels with at most this many rows run in the persistent V-cycle tail kernel
- *   "pdl"        1: stencil kernels use programmatic dependent launch */
+ *   "pdl"        1: stencil kernels use programmatic dependent launch
+ *   "overlap"    1: multi-rank SpMV / GS overlap the halo exchange with interior rows
+ *   "overlap_rows" only levels with at least this many rows overlap (default 2^20) */
 int hpg_set_option(hpg_ctx* ctx, const char* key, int64_t value);
 
 #ifdef __cplusplus

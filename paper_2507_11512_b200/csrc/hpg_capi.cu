@@ -149,6 +149,11 @@ struct Level {
   double* v64 = nullptr;
   float* v32 = nullptr;
   int32_t* inj = nullptr;  // (coarse levels) dst[j] for fine color-0 row j
+  uint8_t* hflag = nullptr;    // rows reading halo slots (multi-rank)
+  int32_t* bnd = nullptr;      // all such rows
+  int64_t nbnd = 0;
+  int32_t* bnd0 = nullptr;     // such rows inside color block 0
+  int64_t nbnd0 = 0;
   std::vector<Nbr> nbrs;
   int32_t* send_idx = nullptr;
   int64_t send_total = 0;
@@ -169,6 +174,10 @@ struct hpg_ctx {
   std::vector<Level> lev;
   cudaStream_t stream = nullptr;
   bool own_stream = true;
+  cudaStream_t halo = nullptr;              // side stream for overlapped halo exchange
+  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+  bool overlap = false;  // measured: no gain over the blocking exchange at 2 and 4 ranks
+  int64_t overlap_rows = 1 << 20;  // only levels this large hide an exchange behind interior rows
   ncclComm_t comm = nullptr;
   int nb = 0;                   // reduction grid
   void* partial = nullptr;      // nb * 64 elements (f64-sized)
@@ -267,6 +276,43 @@ int do_exchange(hpg_ctx* c, int l, int prec, void* v) {
   return HPG_OK;
 }
 
+// Overlapped exchange (ref: comm.py:254-272 exchange_overlapped): pack + NCCL on
+// the halo stream while the compute stream runs rows that read no halo slot and
+// write no send row; exchange_end makes the compute stream wait for the halo.
+int exchange_begin(hpg_ctx* c, int l, int prec, void* v) {
+  Level& L = c->lev[l];
+  CUDA_TRY(cudaEventRecord(c->ev_ready, c->stream));
+  CUDA_TRY(cudaStreamWaitEvent(c->halo, c->ev_ready, 0));
+  if (L.send_total) {
+    if (prec == HPG_F64)
+      hpg::k_pack<double><<<grid_for(L.send_total), 256, 0, c->halo>>>((const double*)v, L.send_idx, L.send_total,
+                                                                       (double*)L.send_buf);
+    else
+      hpg::k_pack<float><<<grid_for(L.send_total), 256, 0, c->halo>>>((const float*)v, L.send_idx, L.send_total,
+                                                                      (float*)L.send_buf);
+    LAUNCH_CHECK();
+    ++c->launches;
+  }
+  const size_t es = esize(prec);
+  NCCL_TRY(ncclGroupStart());
+  for (auto& nb : L.nbrs) {
+    NCCL_TRY(ncclSend((char*)L.send_buf + nb.send_off * es, nb.cnt, nccl_type(prec), nb.rank, c->comm, c->halo));
+    NCCL_TRY(ncclRecv((char*)v + nb.recv_base * es, nb.cnt, nccl_type(prec), nb.rank, c->comm, c->halo));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  CUDA_TRY(cudaEventRecord(c->ev_done, c->halo));
+  return HPG_OK;
+}
+
+int exchange_end(hpg_ctx* c) {
+  CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_done, 0));
+  return HPG_OK;
+}
+
+bool overlapped(hpg_ctx* c, int l) {
+  return c->nranks > 1 && c->overlap && !c->lev[l].nbrs.empty() && c->lev[l].n >= c->overlap_rows;
+}
+
 // rank-ordered allreduce of cnt device scalars in place (ref: comm.py:97-108)
 template <typename T>
 int allreduce_scal(hpg_ctx* c, T* buf, int cnt) {
@@ -279,28 +325,46 @@ int allreduce_scal(hpg_ctx* c, T* buf, int cnt) {
 }
 
 template <typename T>
+int gs_pass_launch(hpg_ctx* c, Level& L, int64_t a, int64_t cnt, const T* r, T* z, const uint8_t* skip,
+                   const int32_t* list) {
+  const T* vals = vals_of<T>(L);
+  if (c->gs_minb == 3)
+    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list));
+  else if (c->gs_minb == 4)
+    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 4>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list));
+  else
+    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 2>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list));
+  ++c->launches;
+  return HPG_OK;
+}
+
+// One forward multicolor sweep (ref: smoother.py:78-114).  Multi-rank: the
+// exchange of z overlaps color 0's interior rows, then color 0's boundary rows,
+// then colors 1.. (block-Jacobi across ranks: one exchange per sweep).
+template <typename T>
 int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
   Timed tm(c, M_GS);
   Timed tm0(c, l == 0 ? M_GS_L0 : -1);  // level-0 sweeps also timed alone (bench roofline)
   Level& L = c->lev[l];
+  const int prec = sizeof(T) == 8 ? HPG_F64 : HPG_F32;
+  int first = 0, rc;
   if (zero) {
     CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n_ext, 4)), 256, z, L.n_ext));
     ++c->launches;
+  } else if (overlapped(c, l) && L.g.ncolors > 0) {
+    if ((rc = exchange_begin(c, l, prec, z))) return rc;
+    const int64_t a = L.g.off[0], b = L.g.off[1];
+    if (b > a && (rc = gs_pass_launch<T>(c, L, a, b - a, r, z, L.hflag, nullptr))) return rc;
+    if ((rc = exchange_end(c))) return rc;
+    if (L.nbnd0 && (rc = gs_pass_launch<T>(c, L, 0, L.nbnd0, r, z, nullptr, L.bnd0))) return rc;
+    first = 1;
   } else {
-    int rc = do_exchange(c, l, sizeof(T) == 8 ? HPG_F64 : HPG_F32, z);
-    if (rc) return rc;
+    if ((rc = do_exchange(c, l, prec, z))) return rc;
   }
-  const T* vals = vals_of<T>(L);
-  for (int col = 0; col < L.g.ncolors; ++col) {
+  for (int col = first; col < L.g.ncolors; ++col) {
     const int64_t a = L.g.off[col], b = L.g.off[col + 1];
     if (b <= a) continue;
-    if (c->gs_minb == 3)
-      CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3>, grid_for(b - a), 256, L.cols, vals, L.ld, a, b - a, r, z));
-    else if (c->gs_minb == 4)
-      CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 4>, grid_for(b - a), 256, L.cols, vals, L.ld, a, b - a, r, z));
-    else
-      CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 2>, grid_for(b - a), 256, L.cols, vals, L.ld, a, b - a, r, z));
-    ++c->launches;
+    if ((rc = gs_pass_launch<T>(c, L, a, b - a, r, z, nullptr, nullptr))) return rc;
   }
   return HPG_OK;
 }
@@ -609,7 +673,8 @@ int gemv_t(hpg_ctx* c, const T* Q, int64_t ldq, int k, const double* y, T* out) 
 
 void free_level(Level& L) {
   for (void* p : {(void*)L.cols, (void*)L.v64, (void*)L.v32, (void*)L.inj, (void*)L.send_idx, L.send_buf,
-                  (void*)L.z64, (void*)L.z32, (void*)L.r64, (void*)L.r32})
+                  (void*)L.z64, (void*)L.z32, (void*)L.r64, (void*)L.r32, (void*)L.hflag, (void*)L.bnd,
+                  (void*)L.bnd0})
     if (p) cudaFree(p);
   L = Level();
 }
@@ -667,6 +732,27 @@ int build_level(hpg_ctx* c, Level& L, const int dims[3]) {
       LAUNCH_CHECK();
     }
   }
+  if (!L.nbrs.empty() && L.n) {
+    // interior / boundary split for the overlapped exchange
+    if ((rc = dmalloc(&L.hflag, L.n, &L.bytes))) return rc;
+    hpg::k_build_halo_flags<<<grid_for(L.n), 256, 0, c->stream>>>(L.g, L.hflag);
+    LAUNCH_CHECK();
+    std::vector<uint8_t> f(L.n);
+    CUDA_TRY(cudaMemcpyAsync(f.data(), L.hflag, L.n, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    std::vector<int32_t> all, c0;
+    for (int64_t i = 0; i < L.n; ++i)
+      if (f[i]) {
+        all.push_back((int32_t)i);
+        if (i < L.g.off[1]) c0.push_back((int32_t)i);
+      }
+    L.nbnd = (int64_t)all.size();
+    L.nbnd0 = (int64_t)c0.size();
+    if ((rc = dmalloc(&L.bnd, std::max<int64_t>(1, L.nbnd) * 4, &L.bytes))) return rc;
+    if ((rc = dmalloc(&L.bnd0, std::max<int64_t>(1, L.nbnd0) * 4, &L.bytes))) return rc;
+    if (L.nbnd) CUDA_TRY(cudaMemcpy(L.bnd, all.data(), L.nbnd * 4, cudaMemcpyHostToDevice));
+    if (L.nbnd0) CUDA_TRY(cudaMemcpy(L.bnd0, c0.data(), L.nbnd0 * 4, cudaMemcpyHostToDevice));
+  }
   if ((rc = dmalloc(&L.z64, L.n_ext * 8, &L.bytes))) return rc;
   if ((rc = dmalloc(&L.z32, L.n_ext * 4, &L.bytes))) return rc;
   if ((rc = dmalloc(&L.r64, L.n * 8, &L.bytes))) return rc;
@@ -680,6 +766,33 @@ int check_prec(int prec) { return prec == HPG_F64 || prec == HPG_F32 ? HPG_OK : 
 int check_level(hpg_ctx* c, int l) {
   if (!c) return fail(HPG_E_ARG, "null context");
   return l >= 0 && l < c->nlev ? HPG_OK : fail(HPG_E_ARG, "level %d out of range", l);
+}
+
+template <typename T>
+int spmv_launch(hpg_ctx* c, Level& L, int64_t cnt, const T* x, T* y, const uint8_t* skip, const int32_t* list) {
+  CUDA_TRY(launch_pdl(c, hpg::k_spmv<T, 0>, grid_for(cnt), 256, (const int32_t*)L.cols, (const T*)vals_of<T>(L),
+                      L.ld, (int64_t)0, cnt, x, (const T*)nullptr, y, (double*)nullptr, skip, list));
+  ++c->launches;
+  return HPG_OK;
+}
+
+// y = A x (ref: krylov.py:83-107); multi-rank: rows without halo columns run
+// while the exchange is in flight, then the boundary rows
+template <typename T>
+int spmv_t(hpg_ctx* c, int l, T* x, T* y) {
+  Level& L = c->lev[l];
+  const int prec = sizeof(T) == 8 ? HPG_F64 : HPG_F32;
+  int rc;
+  if (overlapped(c, l)) {
+    if ((rc = exchange_begin(c, l, prec, x))) return rc;
+    if (L.n && (rc = spmv_launch<T>(c, L, L.n, x, y, L.hflag, nullptr))) return rc;
+    if ((rc = exchange_end(c))) return rc;
+    if (L.nbnd && (rc = spmv_launch<T>(c, L, L.nbnd, x, y, nullptr, L.bnd))) return rc;
+    return HPG_OK;
+  }
+  if ((rc = do_exchange(c, l, prec, x))) return rc;
+  if (!L.n) return HPG_OK;
+  return spmv_launch<T>(c, L, L.n, x, y, nullptr, nullptr);
 }
 
 }  // namespace
@@ -768,6 +881,10 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
   } else if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
     return bail(fail(HPG_E_CUDA, "stream create failed"));
   }
+  if (cudaStreamCreateWithFlags(&c->halo, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(HPG_E_CUDA, "halo stream/event create failed"));
   c->lev.resize(levels);
   dims[0] = local_dims[0];
   dims[1] = local_dims[1];
@@ -792,6 +909,10 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     c->cgs_fused = !(f && f[0] == '0');
     const char* mb = getenv("HPG_GS_MINB");
     if (mb) c->gs_minb = atoi(mb);
+    const char* ov = getenv("HPG_OVERLAP");
+    if (ov) c->overlap = ov[0] != '0';
+    const char* ovr = getenv("HPG_OVERLAP_ROWS");
+    if (ovr) c->overlap_rows = atoll(ovr);
     const char* g = getenv("HPG_PDL");
     c->pdl = !(g && g[0] == '0');
     int per = 0;
@@ -831,6 +952,9 @@ int hpg_destroy(hpg_ctx* c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->comm) ncclCommDestroy(c->comm);
   for (auto e : c->events) cudaEventDestroy(e);
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->halo) cudaStreamDestroy(c->halo);
   if (c->stream && c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return HPG_OK;
@@ -899,19 +1023,7 @@ int hpg_spmv(hpg_ctx* c, int l, int prec, void* x, void* y) {
   int rc = check_level(c, l);
   if (rc || (rc = check_prec(prec))) return rc;
   Timed tm(c, M_SPMV);
-  if ((rc = do_exchange(c, l, prec, x))) return rc;
-  Level& L = c->lev[l];
-  if (!L.n) return HPG_OK;
-  if (prec == HPG_F64)
-    CUDA_TRY(launch_pdl(c, hpg::k_spmv<double, 0>, grid_for(L.n), 256, (const int32_t*)L.cols,
-                        (const double*)L.v64, L.ld, (int64_t)0, L.n, (const double*)x, (const double*)nullptr,
-                        (double*)y, (double*)nullptr));
-  else
-    CUDA_TRY(launch_pdl(c, hpg::k_spmv<float, 0>, grid_for(L.n), 256, (const int32_t*)L.cols, (const float*)L.v32,
-                        L.ld, (int64_t)0, L.n, (const float*)x, (const float*)nullptr, (float*)y,
-                        (double*)nullptr));
-  ++c->launches;
-  return HPG_OK;
+  return prec == HPG_F64 ? spmv_t<double>(c, l, (double*)x, (double*)y) : spmv_t<float>(c, l, (float*)x, (float*)y);
 }
 
 int hpg_exchange(hpg_ctx* c, int l, int prec, void* v) {
@@ -988,7 +1100,8 @@ int hpg_residual(hpg_ctx* c, const double* b, double* x, double* r, double* rho2
   Level& L = c->lev[0];
   double* scal = (double*)c->scal;
   const int nbk = grid_for(L.n);
-  hpg::k_spmv<double, 1><<<nbk, 256, 0, c->stream>>>(L.cols, L.v64, L.ld, 0, L.n, x, b, r, c->spmv_partial);
+  hpg::k_spmv<double, 1><<<nbk, 256, 0, c->stream>>>(L.cols, L.v64, L.ld, 0, L.n, x, b, r, c->spmv_partial, nullptr,
+                                                     nullptr);
   hpg::k_fold<double><<<1, 1024, 0, c->stream>>>(c->spmv_partial, nbk, 1, scal + 200, 0);
   LAUNCH_CHECK();
   c->launches += 2;
@@ -1066,6 +1179,8 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(HPG_E_ARG, "null argument");
   if (!strcmp(key, "cgs_fused")) c->cgs_fused = value != 0;
   else if (!strcmp(key, "pdl")) c->pdl = value != 0;
+  else if (!strcmp(key, "overlap")) c->overlap = value != 0;
+  else if (!strcmp(key, "overlap_rows")) c->overlap_rows = value;
   else if (!strcmp(key, "gs_minb")) c->gs_minb = (int)value;
   else if (!strcmp(key, "tail_rows")) c->tail_rows = value;
   else return fail(HPG_E_ARG, "unknown option %s", key);

@@ -101,16 +101,19 @@ __device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, co
 
 // y[i] = sum_s A[i,s] x[col[i,s]]  for rows [row0, row0+nrows)
 // MODE 0: y = Ax.  MODE 1: y = b - Ax and per-block partial of sum y^2 (fp64 outer residual).
+// skip (nullable): rows with skip[i] != 0 are left alone (interior/boundary
+// split for the overlapped halo exchange); list (nullable): row t is list[t].
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256, 2) k_spmv(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                                  int64_t ld, int64_t row0, int64_t nrows,
                                                  const T* __restrict__ x, const T* __restrict__ b,
-                                                 T* __restrict__ y, double* __restrict__ partial) {
+                                                 T* __restrict__ y, double* __restrict__ partial,
+                                                 const uint8_t* __restrict__ skip, const int32_t* __restrict__ list) {
   pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double sq = 0.0;
-  if (t < nrows) {
-    const int64_t i = row0 + t;
+  const int64_t i = t < nrows ? (list ? (int64_t)list[t] : row0 + t) : 0;
+  if (t < nrows && !(skip && skip[i])) {
     T dd;
     const T acc = row_accumulate<T, false, false, MODE == 0>(cols, vals, ld, i, x, &dd);
     if (MODE == 0) {
@@ -149,11 +152,15 @@ __device__ __forceinline__ void gs_row(const int32_t* __restrict__ cols, const T
 template <typename T, int MINB = 2>
 __global__ void __launch_bounds__(256, MINB) k_gs_pass(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                                     int64_t ld, int64_t row0, int64_t nrows,
-                                                    const T* __restrict__ r, T* z) {
+                                                    const T* __restrict__ r, T* z,
+                                                    const uint8_t* __restrict__ skip,
+                                                    const int32_t* __restrict__ list) {
   pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nrows) return;
-  gs_row<T, false, true>(cols, vals, ld, row0 + t, r, z);
+  const int64_t i = list ? (int64_t)list[t] : row0 + t;
+  if (skip && skip[i]) return;
+  gs_row<T, false, true>(cols, vals, ld, i, r, z);
 }
 
 // Fused residual + injection: for fine color-0 row j < nc,
@@ -424,6 +431,12 @@ __global__ void k_build_inject(Geom gc, int32_t* __restrict__ dst) {
   const int y = (int)((j / gc.lx) % gc.ly);
   const int z = (int)(j / ((int64_t)gc.lx * gc.ly));
   dst[j] = (int32_t)iperm(gc, x, y, z);
+}
+
+// flag[i] = 1 when row i reads a halo slot (ref: problem.py:78-85 halo_row_split)
+__global__ void k_build_halo_flags(Geom g, uint8_t* __restrict__ flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < g.n) flag[i] = row_has_halo(g, i) ? 1 : 0;
 }
 
 __global__ void k_build_send(Geom g, int sx, int sy, int sz, int64_t cnt, int32_t* __restrict__ idx) {
