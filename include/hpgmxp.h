@@ -137,8 +137,20 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
  *   "tail_rows"  levels with at most this many rows run in the persistent V-cycle tail kernel
  *   "pdl"        1: stencil kernels use programmatic dependent launch
  *   "overlap"    1: multi-rank SpMV / GS overlap the halo exchange with interior rows
- *   "overlap_rows" only levels with at least this many rows overlap (default 2^20) */
+ *   "overlap_rows" only levels with at least this many rows overlap (default 2^20)
+ *   "p2p"        1: NVLink peer-memory halo exchange + all-reduce (after hpg_p2p_open) */
 int hpg_set_option(hpg_ctx* ctx, const char* key, int64_t value);
+
+/* NVLink peer memory (csrc/hpg_p2p.cuh).  Collective setup, nranks > 1:
+ *   1. every rank: hpg_p2p_handle -> its symmetric buffer's CUDA IPC handle
+ *      (writes sizeof(cudaIpcMemHandle_t) = 64 bytes);
+ *   2. all-gather the handles (host control plane);
+ *   3. every rank: hpg_p2p_open(all handles, stride) maps the peers, then a
+ *      host barrier before the first exchange.
+ * Afterwards the halo exchange and the rank-ordered reductions run as P2P
+ * kernels over NVLink instead of NCCL (ref: comm.py:97-108, 239-272). */
+int hpg_p2p_handle(hpg_ctx* ctx, void* out, int len);
+int hpg_p2p_open(hpg_ctx* ctx, const void* handles, int stride);
 
 #ifdef __cplusplus
 }

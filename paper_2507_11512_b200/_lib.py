@@ -56,6 +56,8 @@ SIGNATURES = {
     "hpg_launch_count": (_i64, [_p]),
     "hpg_timers": (_i, [_p, _i, _dp]),
     "hpg_set_option": (_i, [_p, C.c_char_p, _i64]),
+    "hpg_p2p_handle": (_i, [_p, _p, _i]),
+    "hpg_p2p_open": (_i, [_p, _p, _i]),
 }
 
 _LIB = None

@@ -16,6 +16,7 @@
 #include "hpg_kernels.cuh"
 #include "hpg_coarse.cuh"
 #include "hpg_cgs.cuh"
+#include "hpg_p2p.cuh"
 
 using hpg::Geom;
 
@@ -155,6 +156,7 @@ struct Level {
   int32_t* bnd0 = nullptr;     // such rows inside color block 0
   int64_t nbnd0 = 0;
   std::vector<Nbr> nbrs;
+  hpg::P2PHalo p2p;            // NVLink peer-memory exchange plan (valid when ctx->p2p)
   int32_t* send_idx = nullptr;
   int64_t send_total = 0;
   void* send_buf = nullptr;
@@ -177,6 +179,15 @@ struct hpg_ctx {
   cudaStream_t halo = nullptr;              // side stream for overlapped halo exchange
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
   bool overlap = false;  // measured: no gain over the blocking exchange at 2 and 4 ranks
+  // NVLink peer memory (hpg_p2p.cuh): symmetric buffer, peers' mappings, sequence numbers
+  bool p2p = false;
+  bool p2p_want = true;
+  char* sym = nullptr;
+  size_t sym_bytes = 0;
+  std::vector<char*> peer_sym;
+  char** d_peer = nullptr;
+  unsigned int* done = nullptr;
+  uint64_t halo_seq = 0, ar_seq = 0;
   int64_t overlap_rows = 1 << 20;  // only levels this large hide an exchange behind interior rows
   ncclComm_t comm = nullptr;
   int nb = 0;                   // reduction grid
@@ -256,6 +267,17 @@ cudaError_t launch_pdl(hpg_ctx* c, void (*k)(KArgs...), int grid, int block, Arg
 int do_exchange(hpg_ctx* c, int l, int prec, void* v) {
   Level& L = c->lev[l];
   if (c->nranks == 1 || L.nbrs.empty()) return HPG_OK;
+  if (c->p2p) {  // one kernel: P2P pack into the neighbours' staging, publish, wait, unpack
+    const uint64_t seq = ++c->halo_seq;
+    const int grid = (int)std::min<int64_t>(296, std::max<int64_t>(1, cdiv(L.p2p.total, 256 * 4)));
+    if (prec == HPG_F64)
+      hpg::k_halo_p2p<double><<<grid, 256, 0, c->stream>>>((double*)v, L.send_idx, L.p2p, seq, c->done);
+    else
+      hpg::k_halo_p2p<float><<<grid, 256, 0, c->stream>>>((float*)v, L.send_idx, L.p2p, seq, c->done);
+    LAUNCH_CHECK();
+    ++c->launches;
+    return HPG_OK;
+  }
   if (L.send_total) {
     if (prec == HPG_F64)
       hpg::k_pack<double><<<grid_for(L.send_total), 256, 0, c->stream>>>((const double*)v, L.send_idx, L.send_total,
@@ -314,9 +336,23 @@ bool overlapped(hpg_ctx* c, int l) {
 }
 
 // rank-ordered allreduce of cnt device scalars in place (ref: comm.py:97-108)
+hpg::P2PAr p2p_ar(hpg_ctx* c) {
+  hpg::P2PAr ar;
+  ar.peer = c->d_peer;
+  ar.me = c->rank;
+  ar.nranks = c->p2p ? c->nranks : 1;
+  return ar;
+}
+
 template <typename T>
 int allreduce_scal(hpg_ctx* c, T* buf, int cnt) {
   if (c->nranks == 1) return HPG_OK;
+  if (c->p2p) {
+    hpg::k_p2p_allreduce<T><<<1, 64, 0, c->stream>>>(buf, cnt, p2p_ar(c), ++c->ar_seq, 0);
+    LAUNCH_CHECK();
+    ++c->launches;
+    return HPG_OK;
+  }
   NCCL_TRY(ncclAllGather(buf, c->gather, cnt, sizeof(T) == 8 ? ncclFloat64 : ncclFloat32, c->comm, c->stream));
   hpg::k_fold_ranks<T><<<1, 64, 0, c->stream>>>((const T*)c->gather, c->nranks, cnt, buf, 0);
   LAUNCH_CHECK();
@@ -502,6 +538,9 @@ int cgs2_fused(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   p.ldq = ldq;
   p.n = c->lev[0].n;
   p.kb = kb;
+  p.ar = p2p_ar(c);
+  p.seq0 = c->ar_seq + 1;
+  if (c->nranks > 1) c->ar_seq += qnext ? 3 : 2;
   if (ldq % 32) return fail(HPG_E_ARG, "basis row stride must be a multiple of 32 elements");
   auto fn = hpg::k_cgs2_fused<T, WR, RPW, U>;
   int per = 0;
@@ -561,7 +600,8 @@ int cgs2_passes(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
 
 template <typename T>
 int cgs2_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext, double* out) {
-  if (c->nranks > 1 && c->cgs_fused && c->lev[0].n % (16 / (int)sizeof(T)) == 0 && ldq % 32 == 0 && k + 1 <= 64) {
+  if (c->nranks > 1 && !c->p2p && c->cgs_fused && c->lev[0].n % (16 / (int)sizeof(T)) == 0 && ldq % 32 == 0 &&
+      k + 1 <= 64) {
     const int kb = k + 1;
     int rc;
     {
@@ -585,7 +625,7 @@ int cgs2_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext, double* out) {
     out[2 * kb] = qnext ? (double)hv[128] : 0.0;
     return HPG_OK;
   }
-  if (c->nranks == 1 && c->cgs_fused && c->lev[0].n % (16 / (int)sizeof(T)) == 0) {
+  if ((c->nranks == 1 || c->p2p) && c->cgs_fused && c->lev[0].n % (16 / (int)sizeof(T)) == 0) {
     const int kb = k + 1;
     int rc;
     {
@@ -795,6 +835,36 @@ int spmv_t(hpg_ctx* c, int l, T* x, T* y) {
   return spmv_launch<T>(c, L, L.n, x, y, nullptr, nullptr);
 }
 
+// Staging layout of rank R's symmetric buffer: per level, per neighbour
+// (ascending rank), 2 parities x count x 8 B, 256-B aligned.  Every rank can
+// evaluate it for every other rank from the geometry alone.
+size_t stage_offset(const hpg_ctx* c, int R, int level, int sender, int64_t* cnt_out) {
+  size_t off = hpg::kSymArSlots + (size_t)2 * c->nranks * hpg::kArSlot * 8;
+  off = (off + 255) & ~(size_t)255;
+  const int coords[3] = {R % c->procs[0], (R / c->procs[0]) % c->procs[1], R / (c->procs[0] * c->procs[1])};
+  for (int l = 0; l < c->nlev; ++l) {
+    int dims[3] = {c->lev[l].g.lx, c->lev[l].g.ly, c->lev[l].g.lz};
+    const Geom g = make_geom(dims, coords, c->procs);
+    struct E {
+      int rank;
+      int64_t cnt;
+    };
+    std::vector<E> es;
+    for (int i = 0; i < 27; ++i)
+      if (g.nbr_rank[i] >= 0) es.push_back({g.nbr_rank[i], hpg::region_size(g, i % 3 - 1, (i / 3) % 3 - 1, i / 9 - 1)});
+    std::sort(es.begin(), es.end(), [](const E& a, const E& b) { return a.rank < b.rank; });
+    for (auto& e : es) {
+      if (l == level && e.rank == sender) {
+        if (cnt_out) *cnt_out = e.cnt;
+        return off;
+      }
+      off += ((size_t)2 * e.cnt * 8 + 255) & ~(size_t)255;
+    }
+  }
+  if (cnt_out) *cnt_out = -1;
+  return off;  // past the end: total size when sender < 0
+}
+
 }  // namespace
 
 // =============================================================== C ABI
@@ -909,6 +979,8 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     c->cgs_fused = !(f && f[0] == '0');
     const char* mb = getenv("HPG_GS_MINB");
     if (mb) c->gs_minb = atoi(mb);
+    const char* pp = getenv("HPG_P2P");
+    if (pp) c->p2p_want = pp[0] != '0';
     const char* ov = getenv("HPG_OVERLAP");
     if (ov) c->overlap = ov[0] != '0';
     const char* ovr = getenv("HPG_OVERLAP_ROWS");
@@ -951,6 +1023,11 @@ int hpg_destroy(hpg_ctx* c) {
     if (p) cudaFree(p);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->comm) ncclCommDestroy(c->comm);
+  for (size_t q = 0; q < c->peer_sym.size(); ++q)
+    if (c->peer_sym[q] && c->peer_sym[q] != c->sym) cudaIpcCloseMemHandle(c->peer_sym[q]);
+  if (c->sym) cudaFree(c->sym);
+  if (c->d_peer) cudaFree(c->d_peer);
+  if (c->done) cudaFree(c->done);
   for (auto e : c->events) cudaEventDestroy(e);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
@@ -1175,11 +1252,75 @@ int hpg_allreduce_host(hpg_ctx* c, double* vals, int n) {
 
 int64_t hpg_launch_count(hpg_ctx* c) { return c ? c->launches : -1; }
 
+int hpg_p2p_handle(hpg_ctx* c, void* out, int len) {
+  if (!c || !out) return fail(HPG_E_ARG, "null argument");
+  if (len < (int)sizeof(cudaIpcMemHandle_t)) return fail(HPG_E_ARG, "need %zu bytes", sizeof(cudaIpcMemHandle_t));
+  if (c->nranks == 1) return fail(HPG_E_ARG, "peer memory needs more than one rank");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (!c->sym) {
+    c->sym_bytes = stage_offset(c, c->rank, -1, -1, nullptr);
+    CUDA_TRY(cudaMalloc((void**)&c->sym, c->sym_bytes));
+    CUDA_TRY(cudaMemset(c->sym, 0, c->sym_bytes));
+    CUDA_TRY(cudaMalloc((void**)&c->done, 64));
+    CUDA_TRY(cudaMemset(c->done, 0, 64));
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->sym));
+  memcpy(out, &h, sizeof h);
+  return HPG_OK;
+}
+
+int hpg_p2p_open(hpg_ctx* c, const void* handles, int stride) {
+  if (!c || !handles) return fail(HPG_E_ARG, "null argument");
+  if (!c->sym) return fail(HPG_E_ARG, "call hpg_p2p_handle first");
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->peer_sym.assign(c->nranks, nullptr);
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) {
+      c->peer_sym[q] = c->sym;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char*)handles + (size_t)q * stride, sizeof h);
+    void* p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->peer_sym[q] = (char*)p;
+  }
+  CUDA_TRY(cudaMalloc((void**)&c->d_peer, sizeof(char*) * c->nranks));
+  CUDA_TRY(cudaMemcpy(c->d_peer, c->peer_sym.data(), sizeof(char*) * c->nranks, cudaMemcpyHostToDevice));
+  for (int l = 0; l < c->nlev; ++l) {
+    Level& L = c->lev[l];
+    memset(&L.p2p, 0, sizeof L.p2p);
+    if ((int)L.nbrs.size() > hpg::kMaxNbr) return fail(HPG_E_ARG, "too many neighbours");
+    L.p2p.nn = (int)L.nbrs.size();
+    for (size_t k = 0; k < L.nbrs.size(); ++k) {
+      const Nbr& nb = L.nbrs[k];
+      int64_t cnt_r = 0, cnt_l = 0;
+      const size_t roff = stage_offset(c, nb.rank, l, c->rank, &cnt_r);
+      const size_t loff = stage_offset(c, c->rank, l, nb.rank, &cnt_l);
+      if (cnt_r != nb.cnt || cnt_l != nb.cnt) return fail(HPG_E_ARG, "asymmetric halo plan");
+      hpg::P2PNbr& d = L.p2p.nb[k];
+      d.remote_stage = c->peer_sym[nb.rank] + roff;
+      d.local_stage = c->sym + loff;
+      d.remote_flag = (uint64_t*)(c->peer_sym[nb.rank] + hpg::kSymHaloFlags) + c->rank;
+      d.local_flag = (const uint64_t*)(c->sym + hpg::kSymHaloFlags) + nb.rank;
+      d.send_off = nb.send_off;
+      d.cnt = nb.cnt;
+      d.recv_base = nb.recv_base;
+      L.p2p.total += nb.cnt;
+    }
+  }
+  c->p2p = c->p2p_want;
+  return HPG_OK;
+}
+
 int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(HPG_E_ARG, "null argument");
   if (!strcmp(key, "cgs_fused")) c->cgs_fused = value != 0;
   else if (!strcmp(key, "pdl")) c->pdl = value != 0;
   else if (!strcmp(key, "overlap")) c->overlap = value != 0;
+  else if (!strcmp(key, "p2p")) c->p2p = value != 0 && !c->peer_sym.empty();
   else if (!strcmp(key, "overlap_rows")) c->overlap_rows = value;
   else if (!strcmp(key, "gs_minb")) c->gs_minb = (int)value;
   else if (!strcmp(key, "tail_rows")) c->tail_rows = value;

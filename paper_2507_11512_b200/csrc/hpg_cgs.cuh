@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "hpg_p2p.cuh"
+
 namespace hpg {
 
 template <typename T>
@@ -77,22 +79,33 @@ struct CgsParams {
   T* scal;         // [0,64) h1, [64,128) h2, [128] beta
   int64_t ldq, n;
   int kb;
+  P2PAr ar;        // multi-rank: NVLink all-reduce between passes (ar.nranks == 1: none)
+  uint64_t seq0;   // sequence number of the first of this call's all-reduces
 };
 
 constexpr int kCgsThreads = 256;
 constexpr int kCgsWarps = kCgsThreads / 32;
 
-// CTA 0 folds the per-CTA partials of cnt outputs into dst (fixed order)
+// CTA 0 folds the per-CTA partials of cnt outputs into dst (fixed order); with
+// several ranks it then all-reduces dst over NVLink in ascending rank order
+// before the optional square root (ref: krylov.py:123, 268; comm.py:97-108).
 template <typename T>
-__device__ __forceinline__ void cgs_fold(const T* partial, int cnt, T* dst, bool do_sqrt) {
+__device__ __forceinline__ void cgs_fold(const T* partial, int cnt, T* dst, bool do_sqrt, const P2PAr& ar,
+                                         uint64_t seq) {
   if (blockIdx.x != 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool multi = ar.nranks > 1;
   for (int j = warp; j < cnt; j += kCgsWarps) {
     T a = T(0);
     for (int b = lane; b < (int)gridDim.x; b += 32) a += __ldcg(partial + (int64_t)j * gridDim.x + b);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) dst[j] = do_sqrt ? sqrt(a) : a;
+    if (lane == 0) dst[j] = (do_sqrt && !multi) ? sqrt(a) : a;
+  }
+  if (multi) {
+    __syncthreads();
+    p2p_allreduce_block<T>(dst, cnt, ar, seq);
+    if (do_sqrt && threadIdx.x == 0) dst[0] = sqrt(dst[0]);
   }
 }
 
@@ -256,7 +269,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
     cgs_store_rows<T, WR, RPW>(acc, p.kb, p.partial, sacc);
   }
   grid.sync();
-  cgs_fold(p.partial, p.kb, p.scal, false);
+  cgs_fold(p.partial, p.kb, p.scal, false, p.ar, p.seq0);
   grid.sync();
   {  // pass B: w -= Q^T h1 ; h2
     T acc[RPW];
@@ -266,7 +279,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
     cgs_store_rows<T, WR, RPW>(acc, p.kb, p.partial, sacc);
   }
   grid.sync();
-  cgs_fold(p.partial, p.kb, p.scal + 64, false);
+  cgs_fold(p.partial, p.kb, p.scal + 64, false, p.ar, p.seq0 + 1);
   grid.sync();
   {  // pass C: w -= Q^T h2 ; beta^2 (row-group-0 warps hold the block's share)
     T acc[RPW];
@@ -277,7 +290,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
   }
   if (p.qnext == nullptr) return;
   grid.sync();
-  cgs_fold(p.partial, 1, p.scal + 128, true);
+  cgs_fold(p.partial, 1, p.scal + 128, true, p.ar, p.seq0 + 2);
   grid.sync();
   // pass D: Q[k+1] = w / beta  (ref: krylov.py:269-273), 16-byte vectors
   using VV = typename Vec16<T>::V;

@@ -31,6 +31,27 @@ class Context:
                                 levels, nu1, nu2, nu_c, uid, C.c_void_p(rt.stream_ptr)))
         self.h = h
         self._info = [self._level_info(l) for l in range(levels)]
+        self.p2p = False
+        if self.nranks > 1:
+            self._open_peer_memory(world)
+
+    def _open_peer_memory(self, world):
+        """Map every rank's symmetric buffer (CUDA IPC over NVLink); NCCL stays as
+        the fallback data path when peer access is unavailable."""
+        import os
+        if os.environ.get("HPG_P2P", "1") == "0":
+            return
+        buf = C.create_string_buffer(64)
+        self.call("hpg_p2p_handle", buf, 64)
+        handles = world.gather(self.rank, bytes(buf.raw))
+        handles = world.broadcast_bytes(handles)
+        blob = C.create_string_buffer(b"".join(handles), 64 * self.nranks)
+        rc = _lib.lib().hpg_p2p_open(self.h, blob, 64)
+        ok = world.all_reduce_sum(self.rank, 1 if rc == 0 else 0) == self.nranks
+        if not ok:
+            self.set_option("p2p", 0)
+        world.barrier()
+        self.p2p = ok
 
     def call(self, name, *args):
         if self.h is None:
