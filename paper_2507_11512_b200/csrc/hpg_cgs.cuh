@@ -117,38 +117,43 @@ __device__ __forceinline__ void cgs_fold(const T* partial, int cnt, T* dst, bool
 // MODE 2: w -= sum_j q_j h_j ; acc[0] += w . w (rg 0)   (pass C)
 // MODE 3: w  = sum_j q_j h_j                           (end-of-cycle basis combination)
 template <typename T, int WR, int RPW, int U, int MODE>
-__device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const T* h, T (&acc)[RPW],
-                                         typename Vec16<T>::V* red) {
+struct CgsStream {
   using V = typename Vec16<T>::V;
-  constexpr int VN = Vec16<T>::N;
-  constexpr int TILE = 32 * VN;  // elements per warp-wide 512 B load
-  constexpr int WE = kCgsWarps / WR;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rg = warp % WR, eg = warp / WR;
-  const int kb = p.kb;
+  static constexpr int VN = Vec16<T>::N;
+  static constexpr int TILE = 32 * VN;  // elements per warp-wide 512 B load
+  static constexpr int WE = kCgsWarps / WR;
+  static constexpr int STEP = WE * U;   // tiles per CTA iteration
+
+  const CgsParams<T>& p;
+  int lane, warp, rg, eg, kb;
+  int64_t t1;
   T hr[RPW];
+
+  __device__ __forceinline__ CgsStream(const CgsParams<T>& p_, const T* h, int64_t t1_) : p(p_), t1(t1_) {
+    lane = threadIdx.x & 31;
+    warp = threadIdx.x >> 5;
+    rg = warp % WR;
+    eg = warp / WR;
+    kb = p.kb;
 #pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const int j = rg + r * WR;
-    hr[r] = (MODE > 0 && j < kb) ? __ldcg(h + j) : T(0);
+    for (int r = 0; r < RPW; ++r) {
+      const int j = rg + r * WR;
+      hr[r] = (MODE > 0 && j < kb) ? __ldcg(h + j) : T(0);
+    }
   }
-  // this CTA's contiguous range of tiles; element group eg takes U of every WE*U
-  const int64_t ntiles = (p.n + TILE - 1) / TILE;
-  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
-  const int64_t t0 = (int64_t)blockIdx.x * per;
-  const int64_t t1 = t0 + per < ntiles ? t0 + per : ntiles;
-  for (int64_t tb = t0; tb < t1; tb += WE * U) {
-    V q[U][RPW];
-    V wv[U];
-    if (tb + WE * U <= t1 && (tb + WE * U) * TILE <= p.n) {  // full iteration: unpredicated loads
+
+  // issue every load of the iteration starting at tile tb (nothing is used yet)
+  __device__ __forceinline__ void load(int64_t tb, V (&q)[U][RPW], V (&wv)[U]) const {
+    if (tb + STEP <= t1 && (tb + STEP) * TILE <= p.n) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t i = (tb + eg * U + u) * TILE + lane * VN;
 #pragma unroll
         for (int r = 0; r < RPW; ++r) {
+          // rows past kb re-read row 0: finite values that are multiplied by hr = 0
+          // or land in unused accumulators -- no select on loaded data
           const int j = rg + r * WR;
           q[u][r] = __ldcs((const V*)(p.Q + (j < kb ? j : 0) * p.ldq + i));
-          if (j >= kb) q[u][r] = V{};
         }
         if (MODE != 3) wv[u] = __ldcg((const V*)(p.w + i));
       }
@@ -166,6 +171,10 @@ __device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const T* h, T (&
         wv[u] = (in && MODE != 3) ? __ldcg((const V*)(p.w + i)) : V{};
       }
     }
+  }
+
+  // consume one iteration (block-uniform: contains barriers when WR > 1)
+  __device__ __forceinline__ void process(int64_t tb, V (&q)[U][RPW], V (&wv)[U], T (&acc)[RPW], V* red) const {
     if (MODE > 0) {
       if (WR > 1) {
         // this warp's share of the correction, then the sum over the row group (fixed order)
@@ -230,6 +239,39 @@ __device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const T* h, T (&
         for (int c = 0; c < VN; ++c) acc[0] = fma(vget<T>(wv[u], c), vget<T>(wv[u], c), acc[0]);
     }
   }
+};
+
+// One streaming pass over this CTA's contiguous range of tiles.  PIPE (wide
+// bases): software pipelined, the loads of iteration i+1 are in flight while
+// iteration i is consumed (two register sets, alternating); narrow bases use
+// one larger register set (U tiles) instead -- measured faster for kb <= 16.
+template <typename T, int WR, int RPW, int U, int MODE, bool PIPE>
+__device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const T* h, T (&acc)[RPW],
+                                         typename Vec16<T>::V* red) {
+  using S = CgsStream<T, WR, RPW, U, MODE>;
+  using V = typename S::V;
+  const int64_t ntiles = (p.n + S::TILE - 1) / S::TILE;
+  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * per;
+  const int64_t t1 = t0 + per < ntiles ? t0 + per : ntiles;
+  const S st(p, h, t1);
+  if (!PIPE) {  // one register set: load, then consume
+    for (int64_t tb = t0; tb < t1; tb += S::STEP) {
+      V q[U][RPW], wv[U];
+      st.load(tb, q, wv);
+      st.process(tb, q, wv, acc, red);
+    }
+    return;
+  }
+  V qa[U][RPW], wa[U], qb[U][RPW], wb[U];
+  if (t0 < t1) st.load(t0, qa, wa);
+  for (int64_t tb = t0; tb < t1; tb += 2 * S::STEP) {
+    st.load(tb + S::STEP, qb, wb);
+    st.process(tb, qa, wa, acc, red);
+    if (tb + S::STEP >= t1) break;
+    st.load(tb + 2 * S::STEP, qa, wa);
+    st.process(tb + S::STEP, qb, wb, acc, red);
+  }
 }
 
 // rows -> partial[j][block]: lane reduce per warp, then element groups added in order
@@ -265,7 +307,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
     T acc[RPW];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) acc[r] = T(0);
-    cgs_pass<T, WR, RPW, U, 0>(p, nullptr, acc, red);
+    cgs_pass<T, WR, RPW, U, 0, (RPW >= 4)>(p, nullptr, acc, red);
     cgs_store_rows<T, WR, RPW>(acc, p.kb, p.partial, sacc);
   }
   grid.sync();
@@ -275,7 +317,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
     T acc[RPW];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) acc[r] = T(0);
-    cgs_pass<T, WR, RPW, U, 1>(p, p.scal, acc, red);
+    cgs_pass<T, WR, RPW, U, 1, (RPW >= 4)>(p, p.scal, acc, red);
     cgs_store_rows<T, WR, RPW>(acc, p.kb, p.partial, sacc);
   }
   grid.sync();
@@ -285,7 +327,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
     T acc[RPW];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) acc[r] = T(0);
-    cgs_pass<T, WR, RPW, U, 2>(p, p.scal + 64, acc, red);
+    cgs_pass<T, WR, RPW, U, 2, (RPW >= 4)>(p, p.scal + 64, acc, red);
     cgs_store_rows<T, WR, RPW>(acc, 1, p.partial, sacc);
   }
   if (p.qnext == nullptr) return;
@@ -318,7 +360,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs_onepass(const __grid_con
   T acc[RPW];
 #pragma unroll
   for (int r = 0; r < RPW; ++r) acc[r] = T(0);
-  cgs_pass<T, WR, RPW, U, MODE>(p, h, acc, red);
+  cgs_pass<T, WR, RPW, U, MODE, (RPW >= 4)>(p, h, acc, red);
   cgs_store_rows<T, WR, RPW>(acc, MODE == 2 ? 1 : p.kb, p.partial, sacc);
 }
 
@@ -329,7 +371,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_gemv_combine(const __grid_co
   using V = typename Vec16<T>::V;
   __shared__ V red[WR > 1 ? U * kCgsWarps * 32 : 1];
   T acc[RPW];
-  cgs_pass<T, WR, RPW, U, 3>(p, p.scal, acc, red);
+  cgs_pass<T, WR, RPW, U, 3, (RPW >= 4)>(p, p.scal, acc, red);
 }
 
 }  // namespace hpg
