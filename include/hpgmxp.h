@@ -109,6 +109,10 @@ int hpg_vcycle(hpg_ctx* ctx, int prec, const void* r, void* z_ext);
  * 266-273).  Synchronises.  Reductions are rank-ordered (ref: comm.py:97-108). */
 int hpg_cgs2(hpg_ctx* ctx, int prec, void* Q, int64_t ldq, int k, void* w, void* q_next,
              double* host_out);
+/* The same step split in two: _begin enqueues everything (no host wait),
+ * _end blocks until (h1, h2, beta) of the step in flight are on the host. */
+int hpg_cgs2_begin(hpg_ctx* ctx, int prec, void* Q, int64_t ldq, int k, void* w, void* q_next);
+int hpg_cgs2_end(hpg_ctx* ctx, double* host_out);
 /* out = Q[0:k]^T y  (y given on the host in fp64, narrowed to prec first;
  * ref: krylov.py:288-289) */
 int hpg_gemv_combine(hpg_ctx* ctx, int prec, const void* Q, int64_t ldq, int k,

@@ -46,6 +46,8 @@ SIGNATURES = {
     "hpg_prolong": (_i, [_p, _i, _i, _p, _p]),
     "hpg_vcycle": (_i, [_p, _i, _p, _p]),
     "hpg_cgs2": (_i, [_p, _i, _p, _i64, _i, _p, _p, _dp]),
+    "hpg_cgs2_begin": (_i, [_p, _i, _p, _i64, _i, _p, _p]),
+    "hpg_cgs2_end": (_i, [_p, _dp]),
     "hpg_gemv_combine": (_i, [_p, _i, _p, _i64, _i, _dp, _p]),
     "hpg_axpy_mixed": (_i, [_p, _i, _p, _p, _i64]),
     "hpg_residual": (_i, [_p, _p, _p, _p, _dp]),

@@ -178,6 +178,9 @@ struct hpg_ctx {
   bool own_stream = true;
   cudaStream_t halo = nullptr;              // side stream for overlapped halo exchange
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+  cudaEvent_t ev_cgs = nullptr;             // (h1, h2, beta) landed in pinned memory
+  int cgs_pending_kb = 0, cgs_pending_es = 4;
+  bool cgs_pending_norm = false;
   bool overlap = false;  // measured: no gain over the blocking exchange at 2 and 4 ranks
   // NVLink peer memory (hpg_p2p.cuh): symmetric buffer, peers' mappings, sequence numbers
   bool p2p = false;
@@ -598,14 +601,19 @@ int cgs2_passes(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   return HPG_OK;
 }
 
+// Enqueue one CGS2 step (+ norm + normalise when qnext) and the async copy of
+// (h1, h2, beta) to pinned host memory; cgs2_finish waits for it.  Splitting
+// the two lets the host enqueue the next Arnoldi step's V-cycle and SpMV
+// before it blocks on this step's coefficients.
 template <typename T>
-int cgs2_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext, double* out) {
-  if (c->nranks > 1 && !c->p2p && c->cgs_fused && c->lev[0].n % (16 / (int)sizeof(T)) == 0 && ldq % 32 == 0 &&
-      k + 1 <= 64) {
-    const int kb = k + 1;
-    int rc;
-    {
-      Timed tm(c, M_ORTHO);
+int cgs2_launch_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext) {
+  const int kb = k + 1;
+  if (kb > 64) return fail(HPG_E_UNSUPPORTED, "restart basis of %d vectors exceeds 64", kb);
+  const bool vec_ok = c->lev[0].n % (16 / (int)sizeof(T)) == 0 && ldq % 32 == 0;
+  int rc;
+  {
+    Timed tm(c, M_ORTHO);
+    if (c->nranks > 1 && !c->p2p && c->cgs_fused && vec_ok) {
       if (kb <= 1) rc = cgs2_passes<T, 1, 1, 8>(c, Q, ldq, kb, w, qnext);
       else if (kb <= 2) rc = cgs2_passes<T, 2, 1, 8>(c, Q, ldq, kb, w, qnext);
       else if (kb <= 4) rc = cgs2_passes<T, 4, 1, 8>(c, Q, ldq, kb, w, qnext);
@@ -613,64 +621,54 @@ int cgs2_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext, double* out) {
       else if (kb <= 16) rc = cgs2_passes<T, 8, 2, 4>(c, Q, ldq, kb, w, qnext);
       else if (kb <= 32) rc = cgs2_passes<T, 8, 4, 2>(c, Q, ldq, kb, w, qnext);
       else rc = cgs2_passes<T, 8, 8, 1>(c, Q, ldq, kb, w, qnext);
-      if (rc) return rc;
-    }
-    CUDA_TRY(cudaMemcpyAsync(c->pinned, c->scal, 129 * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    const T* hv = (const T*)c->pinned;
-    for (int j = 0; j < kb; ++j) {
-      out[j] = (double)hv[j];
-      out[kb + j] = (double)hv[64 + j];
-    }
-    out[2 * kb] = qnext ? (double)hv[128] : 0.0;
-    return HPG_OK;
-  }
-  if ((c->nranks == 1 || c->p2p) && c->cgs_fused && c->lev[0].n % (16 / (int)sizeof(T)) == 0) {
-    const int kb = k + 1;
-    int rc;
-    {
-      Timed tm(c, M_ORTHO);
+    } else if ((c->nranks == 1 || c->p2p) && c->cgs_fused && vec_ok) {
       if (kb <= 1) rc = cgs2_fused<T, 1, 1, 8>(c, Q, ldq, kb, w, qnext);
       else if (kb <= 2) rc = cgs2_fused<T, 2, 1, 8>(c, Q, ldq, kb, w, qnext);
       else if (kb <= 4) rc = cgs2_fused<T, 4, 1, 8>(c, Q, ldq, kb, w, qnext);
       else if (kb <= 8) rc = cgs2_fused<T, 4, 2, 4>(c, Q, ldq, kb, w, qnext);
       else if (kb <= 16) rc = cgs2_fused<T, 8, 2, 4>(c, Q, ldq, kb, w, qnext);
       else if (kb <= 32) rc = cgs2_fused<T, 8, 4, 2>(c, Q, ldq, kb, w, qnext);
-      else if (kb <= 64) rc = cgs2_fused<T, 8, 8, 1>(c, Q, ldq, kb, w, qnext);
-      else return fail(HPG_E_UNSUPPORTED, "restart basis of %d vectors exceeds 64", kb);
-      if (rc) return rc;
+      else rc = cgs2_fused<T, 8, 8, 1>(c, Q, ldq, kb, w, qnext);
+    } else {
+      if (kb <= 4) rc = cgs2_kb<T, 4>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 8) rc = cgs2_kb<T, 8>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 16) rc = cgs2_kb<T, 16>(c, Q, ldq, kb, w, qnext);
+      else if (kb <= 32) rc = cgs2_kb<T, 32>(c, Q, ldq, kb, w, qnext);
+      else rc = cgs2_kb<T, 64>(c, Q, ldq, kb, w, qnext);
     }
-    CUDA_TRY(cudaMemcpyAsync(c->pinned, c->scal, 129 * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    const T* hv = (const T*)c->pinned;
-    for (int j = 0; j < kb; ++j) {
-      out[j] = (double)hv[j];
-      out[kb + j] = (double)hv[64 + j];
-    }
-    out[2 * kb] = qnext ? (double)hv[128] : 0.0;
-    return HPG_OK;
-  }
-  const int kb = k + 1;
-  int rc;
-  {
-  Timed tm(c, M_ORTHO);
-  if (kb <= 4) rc = cgs2_kb<T, 4>(c, Q, ldq, kb, w, qnext);
-  else if (kb <= 8) rc = cgs2_kb<T, 8>(c, Q, ldq, kb, w, qnext);
-  else if (kb <= 16) rc = cgs2_kb<T, 16>(c, Q, ldq, kb, w, qnext);
-  else if (kb <= 32) rc = cgs2_kb<T, 32>(c, Q, ldq, kb, w, qnext);
-  else if (kb <= 64) rc = cgs2_kb<T, 64>(c, Q, ldq, kb, w, qnext);
-  else return fail(HPG_E_UNSUPPORTED, "restart basis of %d vectors exceeds 64", kb);
-  if (rc) return rc;
+    if (rc) return rc;
   }
   CUDA_TRY(cudaMemcpyAsync(c->pinned, c->scal, 129 * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  const T* hv = (const T*)c->pinned;
-  for (int j = 0; j < kb; ++j) {
-    out[j] = (double)hv[j];
-    out[kb + j] = (double)hv[64 + j];
-  }
-  out[2 * kb] = qnext ? (double)hv[128] : 0.0;
+  CUDA_TRY(cudaEventRecord(c->ev_cgs, c->stream));
+  c->cgs_pending_kb = kb;
+  c->cgs_pending_es = (int)sizeof(T);
+  c->cgs_pending_norm = qnext != nullptr;
   return HPG_OK;
+}
+
+int cgs2_finish(hpg_ctx* c, double* out) {
+  if (c->cgs_pending_kb <= 0) return fail(HPG_E_ARG, "no CGS2 step in flight");
+  CUDA_TRY(cudaEventSynchronize(c->ev_cgs));
+  const int kb = c->cgs_pending_kb;
+  for (int j = 0; j < kb; ++j) {
+    if (c->cgs_pending_es == 8) {
+      out[j] = ((const double*)c->pinned)[j];
+      out[kb + j] = ((const double*)c->pinned)[64 + j];
+    } else {
+      out[j] = ((const float*)c->pinned)[j];
+      out[kb + j] = ((const float*)c->pinned)[64 + j];
+    }
+  }
+  out[2 * kb] = !c->cgs_pending_norm ? 0.0
+                : c->cgs_pending_es == 8 ? ((const double*)c->pinned)[128] : ((const float*)c->pinned)[128];
+  c->cgs_pending_kb = 0;
+  return HPG_OK;
+}
+
+template <typename T>
+int cgs2_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext, double* out) {
+  int rc = cgs2_launch_t<T>(c, Q, ldq, k, w, qnext);
+  return rc ? rc : cgs2_finish(c, out);
 }
 
 template <typename T, int WR, int RPW, int U>
@@ -953,7 +951,8 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
   }
   if (cudaStreamCreateWithFlags(&c->halo, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess)
+      cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_cgs, cudaEventDisableTiming) != cudaSuccess)
     return bail(fail(HPG_E_CUDA, "halo stream/event create failed"));
   c->lev.resize(levels);
   dims[0] = local_dims[0];
@@ -1031,6 +1030,7 @@ int hpg_destroy(hpg_ctx* c) {
   for (auto e : c->events) cudaEventDestroy(e);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->ev_cgs) cudaEventDestroy(c->ev_cgs);
   if (c->halo) cudaStreamDestroy(c->halo);
   if (c->stream && c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1145,6 +1145,19 @@ int hpg_cgs2(hpg_ctx* c, int prec, void* Q, int64_t ldq, int k, void* w, void* q
   if (k < 0) return fail(HPG_E_ARG, "bad k");
   return prec == HPG_F64 ? cgs2_t<double>(c, (double*)Q, ldq, k, (double*)w, (double*)qnext, out)
                          : cgs2_t<float>(c, (float*)Q, ldq, k, (float*)w, (float*)qnext, out);
+}
+
+int hpg_cgs2_begin(hpg_ctx* c, int prec, void* Q, int64_t ldq, int k, void* w, void* qnext) {
+  int rc = check_level(c, 0);
+  if (rc || (rc = check_prec(prec))) return rc;
+  if (k < 0) return fail(HPG_E_ARG, "bad k");
+  return prec == HPG_F64 ? cgs2_launch_t<double>(c, (double*)Q, ldq, k, (double*)w, (double*)qnext)
+                         : cgs2_launch_t<float>(c, (float*)Q, ldq, k, (float*)w, (float*)qnext);
+}
+
+int hpg_cgs2_end(hpg_ctx* c, double* out) {
+  if (!c) return fail(HPG_E_ARG, "null context");
+  return cgs2_finish(c, out);
 }
 
 int hpg_gemv_combine(hpg_ctx* c, int prec, const void* Q, int64_t ldq, int k, const double* y, void* out) {

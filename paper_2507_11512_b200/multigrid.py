@@ -44,7 +44,7 @@ class MgHierarchy:
     rank: int = 0
     ctx: object = field(default=None, repr=False)
 
-    def apply(self, r, tally=None, out=None):
+    def apply(self, r, tally=None, out=None, count=True):
         """One V-cycle from the finest level; precision follows r's dtype (ref: multigrid.py:49-51).
 
         Returns the level-0 workspace view (or ``out[:n]`` when given, out having
@@ -56,18 +56,26 @@ class MgHierarchy:
         A = lv.A_lo if lo else lv.A_hi
         z = out if out is not None else (lv.z_lo if lo else lv.z_hi)
         self.ctx.call("hpg_vcycle", A.prec, _lib.ptr(r), _lib.ptr(z))
-        if tally is not None:
+        if tally is not None and count:
             count_vcycle(self, tally, A.dtype)
         return z[:A.n_rows]
 
     def preconditioner(self, tally=None):
         """Callable precond(r, out=None) for gmres_solve (writes into out when given)."""
         hier = self
+        last = {}
 
-        def precond(r, out=None):
-            return hier.apply(r, tally, out)
+        def precond(r, out=None, count=True):
+            last["dtype"] = np.float32 if r.dtype.itemsize == 4 else np.float64
+            return hier.apply(r, tally, out, count)
+
+        def account():
+            """Tally one V-cycle (for applications issued with count=False)."""
+            if tally is not None:
+                count_vcycle(hier, tally, last.get("dtype", np.float64))
 
         precond.accepts_out = True
+        precond.account = account
         return precond
 
     def close(self):
