@@ -367,7 +367,10 @@ template <typename T>
 int gs_pass_launch(hpg_ctx* c, Level& L, int64_t a, int64_t cnt, const T* r, T* z, const uint8_t* skip,
                    const int32_t* list) {
   const T* vals = vals_of<T>(L);
-  if (c->gs_minb == 3)
+  if (skip || list)
+    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3, true>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip,
+                        list));
+  else if (c->gs_minb == 3)
     CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list));
   else if (c->gs_minb == 4)
     CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 4>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list));
@@ -648,7 +651,8 @@ int cgs2_launch_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext) {
 
 int cgs2_finish(hpg_ctx* c, double* out) {
   if (c->cgs_pending_kb <= 0) return fail(HPG_E_ARG, "no CGS2 step in flight");
-  CUDA_TRY(cudaEventSynchronize(c->ev_cgs));
+  if (getenv("HPG_CGS_STREAMSYNC")) CUDA_TRY(cudaStreamSynchronize(c->stream));
+  else CUDA_TRY(cudaEventSynchronize(c->ev_cgs));
   const int kb = c->cgs_pending_kb;
   for (int j = 0; j < kb; ++j) {
     if (c->cgs_pending_es == 8) {
@@ -808,8 +812,13 @@ int check_level(hpg_ctx* c, int l) {
 
 template <typename T>
 int spmv_launch(hpg_ctx* c, Level& L, int64_t cnt, const T* x, T* y, const uint8_t* skip, const int32_t* list) {
-  CUDA_TRY(launch_pdl(c, hpg::k_spmv<T, 0>, grid_for(cnt), 256, (const int32_t*)L.cols, (const T*)vals_of<T>(L),
-                      L.ld, (int64_t)0, cnt, x, (const T*)nullptr, y, (double*)nullptr, skip, list));
+  if (skip || list)
+    CUDA_TRY(launch_pdl(c, hpg::k_spmv<T, 0, true>, grid_for(cnt), 256, (const int32_t*)L.cols,
+                        (const T*)vals_of<T>(L), L.ld, (int64_t)0, cnt, x, (const T*)nullptr, y, (double*)nullptr,
+                        skip, list));
+  else
+    CUDA_TRY(launch_pdl(c, hpg::k_spmv<T, 0>, grid_for(cnt), 256, (const int32_t*)L.cols, (const T*)vals_of<T>(L),
+                        L.ld, (int64_t)0, cnt, x, (const T*)nullptr, y, (double*)nullptr, skip, list));
   ++c->launches;
   return HPG_OK;
 }

@@ -103,7 +103,7 @@ __device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, co
 // MODE 0: y = Ax.  MODE 1: y = b - Ax and per-block partial of sum y^2 (fp64 outer residual).
 // skip (nullable): rows with skip[i] != 0 are left alone (interior/boundary
 // split for the overlapped halo exchange); list (nullable): row t is list[t].
-template <typename T, int MODE>
+template <typename T, int MODE, bool SPLIT = false>
 __global__ void __launch_bounds__(256, 2) k_spmv(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                                  int64_t ld, int64_t row0, int64_t nrows,
                                                  const T* __restrict__ x, const T* __restrict__ b,
@@ -112,8 +112,13 @@ __global__ void __launch_bounds__(256, 2) k_spmv(const int32_t* __restrict__ col
   pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double sq = 0.0;
-  const int64_t i = t < nrows ? (list ? (int64_t)list[t] : row0 + t) : 0;
-  if (t < nrows && !(skip && skip[i])) {
+  int64_t i = row0 + t;
+  bool active = t < nrows;
+  if (SPLIT && active) {
+    if (list) i = list[t];
+    if (skip && skip[i]) active = false;
+  }
+  if (active) {
     T dd;
     const T acc = row_accumulate<T, false, false, MODE == 0>(cols, vals, ld, i, x, &dd);
     if (MODE == 0) {
@@ -149,7 +154,10 @@ __device__ __forceinline__ void gs_row(const int32_t* __restrict__ cols, const T
   z[i] = div_rn(sub_rn(ldv<COHERENT>(r + i), acc), d);
 }
 
-template <typename T, int MINB = 2>
+// SPLIT: rows may be skipped (skip[i] != 0) or taken from a list (interior /
+// boundary halves of color 0 around an overlapped exchange); the plain
+// instantiation is the hot path and carries neither.
+template <typename T, int MINB = 2, bool SPLIT = false>
 __global__ void __launch_bounds__(256, MINB) k_gs_pass(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                                     int64_t ld, int64_t row0, int64_t nrows,
                                                     const T* __restrict__ r, T* z,
@@ -158,8 +166,11 @@ __global__ void __launch_bounds__(256, MINB) k_gs_pass(const int32_t* __restrict
   pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nrows) return;
-  const int64_t i = list ? (int64_t)list[t] : row0 + t;
-  if (skip && skip[i]) return;
+  int64_t i = row0 + t;
+  if (SPLIT) {
+    if (list) i = list[t];
+    if (skip && skip[i]) return;
+  }
   gs_row<T, false, true>(cols, vals, ld, i, r, z);
 }
 
