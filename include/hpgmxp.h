@@ -58,6 +58,13 @@ int hpg_host_level(const int local_dims[3], const int rank_coords[3], const int 
 int64_t hpg_host_send_rows(const int local_dims[3], const int rank_coords[3], const int proc_dims[3],
                            int sx, int sy, int sz, int64_t* rows);
 
+/* Byte offset, inside `receiver`'s peer-memory symmetric buffer, of the staging
+ * region where `sender`'s halo messages for `level` land (count receives the
+ * element count, -1 if the two are not neighbours; sender < 0 returns the
+ * buffer size).  Host-only, used by the CPU layout tests. */
+int64_t hpg_host_stage_offset(const int local_dims[3], const int proc_dims[3], int levels, int receiver,
+                              int level, int sender, int64_t* count);
+
 /* ---- lifecycle ---- */
 
 /* ncclGetUniqueId into out[0..127] (rank 0 calls it, then broadcasts). */

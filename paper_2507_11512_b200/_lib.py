@@ -32,6 +32,7 @@ SIGNATURES = {
     "hpg_last_error": (C.c_char_p, []),
     "hpg_host_level": (_i, [_ip, _ip, _ip, _dp, _i32p, _i32p, _i32p, _i64p, _i]),
     "hpg_host_send_rows": (_i64, [_ip, _ip, _ip, _i, _i, _i, _i64p]),
+    "hpg_host_stage_offset": (_i64, [_ip, _ip, _i, _i, _i, _i, _i64p]),
     "hpg_nccl_unique_id": (_i, [_p, _i]),
     "hpg_create": (_i, [C.POINTER(_p), _i, _i, _i, _ip, _ip, _i, _i, _i, _i, _p, _p]),
     "hpg_destroy": (_i, [_p]),

@@ -845,13 +845,15 @@ int spmv_t(hpg_ctx* c, int l, T* x, T* y) {
 // Staging layout of rank R's symmetric buffer: per level, per neighbour
 // (ascending rank), 2 parities x count x 8 B, 256-B aligned.  Every rank can
 // evaluate it for every other rank from the geometry alone.
-size_t stage_offset(const hpg_ctx* c, int R, int level, int sender, int64_t* cnt_out) {
-  size_t off = hpg::kSymArSlots + (size_t)2 * c->nranks * hpg::kArSlot * 8;
+size_t stage_offset_geo(const int procs[3], const int local0[3], int nlev, int R, int level, int sender,
+                        int64_t* cnt_out) {
+  const int nranks = procs[0] * procs[1] * procs[2];
+  size_t off = hpg::kSymArSlots + (size_t)2 * nranks * hpg::kArSlot * 8;
   off = (off + 255) & ~(size_t)255;
-  const int coords[3] = {R % c->procs[0], (R / c->procs[0]) % c->procs[1], R / (c->procs[0] * c->procs[1])};
-  for (int l = 0; l < c->nlev; ++l) {
-    int dims[3] = {c->lev[l].g.lx, c->lev[l].g.ly, c->lev[l].g.lz};
-    const Geom g = make_geom(dims, coords, c->procs);
+  const int coords[3] = {R % procs[0], (R / procs[0]) % procs[1], R / (procs[0] * procs[1])};
+  int dims[3] = {local0[0], local0[1], local0[2]};
+  for (int l = 0; l < nlev; ++l) {
+    const Geom g = make_geom(dims, coords, procs);
     struct E {
       int rank;
       int64_t cnt;
@@ -867,9 +869,18 @@ size_t stage_offset(const hpg_ctx* c, int R, int level, int sender, int64_t* cnt
       }
       off += ((size_t)2 * e.cnt * 8 + 255) & ~(size_t)255;
     }
+    for (int a = 0; a < 3; ++a) dims[a] /= 2;
   }
   if (cnt_out) *cnt_out = -1;
   return off;  // past the end: total size when sender < 0
+}
+
+// Staging layout of rank R's symmetric buffer: per level, per neighbour
+// (ascending rank), 2 parities x count x 8 B, 256-B aligned.  Every rank can
+// evaluate it for every other rank from the geometry alone.
+size_t stage_offset(const hpg_ctx* c, int R, int level, int sender, int64_t* cnt_out) {
+  const int local0[3] = {c->lev[0].g.lx, c->lev[0].g.ly, c->lev[0].g.lz};
+  return stage_offset_geo(c->procs, local0, c->nlev, R, level, sender, cnt_out);
 }
 
 }  // namespace
@@ -911,6 +922,11 @@ int64_t hpg_host_send_rows(const int local_dims[3], const int rank_coords[3], co
   if (rows)
     for (int64_t p = 0; p < cnt; ++p) rows[p] = hpg::send_row(g, sx, sy, sz, p);
   return cnt;
+}
+
+int64_t hpg_host_stage_offset(const int local_dims[3], const int proc_dims[3], int levels, int receiver, int level,
+                              int sender, int64_t* count) {
+  return (int64_t)stage_offset_geo(proc_dims, local_dims, levels, receiver, level, sender, count);
 }
 
 int hpg_nccl_unique_id(void* out, int len) {

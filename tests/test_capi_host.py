@@ -62,3 +62,46 @@ def test_host_structure_matches_reference(case):
                 np.testing.assert_array_equal(rows, g[p + f"send_{nb}"])
             if li + 1 < levels:
                 dom = dom.coarsen()
+
+
+@pytest.mark.parametrize("local,ranks,levels", [((8, 8, 8), 8, 4), ((16, 16, 16), 8, 4), ((4, 4, 4), 12, 2),
+                                                ((256, 256, 256), 8, 4), ((8, 8, 8), 27, 3)])
+def test_peer_memory_staging_layout(local, ranks, levels):
+    """Every rank's P2P staging regions (csrc/hpg_p2p.cuh): one per (level, neighbour),
+    sized to the neighbour's send list, disjoint, inside the buffer -- checked for the
+    8-GPU 2x2x2 grid the driver runs (and 12 / 27 ranks) without GPUs."""
+    import ctypes as C
+    L = _lib.lib()
+    gp = GlobalProblem.from_local(*local, ranks)
+    procs = (gp.npx, gp.npy, gp.npz)
+    cnt = C.c_int64()
+    for R in range(ranks):
+        total = L.hpg_host_stage_offset(_lib.ints(*local), _lib.ints(*procs), levels, R, 0, -1, None)
+        spans = []
+        dom = gp.domain(R)
+        for lev in range(levels):
+            plan = HaloPlan.__new__(HaloPlan)
+            plan.domain = dom
+            sends_into_R = {}
+            for S in dom.neighbor_ranks():
+                sd = gp.domain(S)
+                for _ in range(lev):
+                    sd = sd.coarsen()
+                p2 = HaloPlan.__new__(HaloPlan)
+                p2.domain = sd
+                sends_into_R[S] = len(p2.send_rows()[R])
+            for S in range(ranks):
+                off = L.hpg_host_stage_offset(_lib.ints(*local), _lib.ints(*procs), levels, R, lev, S,
+                                              C.byref(cnt))
+                if S in sends_into_R:
+                    assert cnt.value == sends_into_R[S], (R, S, lev)
+                    spans.append((off, off + 2 * cnt.value * 8))
+                else:
+                    assert cnt.value == -1
+            if lev + 1 < levels:
+                dom = dom.coarsen()
+        spans.sort()
+        assert spans[0][0] >= 64 * 1024
+        for a, b in zip(spans, spans[1:]):
+            assert a[1] <= b[0]
+        assert spans[-1][1] <= total
