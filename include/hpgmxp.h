@@ -87,6 +87,12 @@ int hpg_level_info(hpg_ctx* ctx, int level, int64_t* info, int ninfo);
 /* Copy a device level back in the reference layout (host buffers [n][27]). */
 int hpg_export_level(hpg_ctx* ctx, int level, double* values, int32_t* col_idx,
                      int32_t* row_nnz, int32_t* diag_pos);
+/* Replace level `level`'s (greedy, closed-form) coloring by an explicit one --
+ * e.g. JPL (ref: coloring.py:56-70): perm[new row] = natural row, rows sorted by
+ * (color, natural); offsets[0..ncolors] the color blocks.  Rebuilds the level's
+ * ELL, send lists and the injection maps touching it (general gather kernels
+ * then serve restriction / prolongation).  Synchronises. */
+int hpg_set_coloring(hpg_ctx* ctx, int level, int ncolors, const int64_t* offsets, const int64_t* perm);
 /* Injection map f2c of coarse level `level` (>=1) into its parent (ref: multigrid.py:87-99). */
 int hpg_export_f2c(hpg_ctx* ctx, int level, int64_t* f2c);
 

@@ -47,11 +47,74 @@ def greedy_coloring(lx, ly, lz):
                     iperm=iperm)
 
 
+def _local_neighbours(lx, ly, lz, rows):
+    """[len(rows), 26] natural indices of the in-box 27-point neighbours (-1: none), ascending."""
+    x, y, z = rows % lx, (rows // lx) % ly, rows // (lx * ly)
+    out = np.full((len(rows), 26), -1, dtype=np.int64)
+    s = 0
+    for dz in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                if dx == dy == dz == 0:
+                    continue
+                ax, ay, az = x + dx, y + dy, z + dz
+                ok = (ax >= 0) & (ax < lx) & (ay >= 0) & (ay < ly) & (az >= 0) & (az < lz)
+                out[ok, s] = (ax + lx * (ay + ly * az))[ok]
+                s += 1
+    return out
+
+
+def jpl_coloring(lx, ly, lz, seed=0, chunk=1 << 20):
+    """Jones-Plassmann-Luby coloring, vectorised, identical to the reference's
+    (ref: coloring.py:56-70): each round draws rng.random(n); a remaining row is
+    selected when (w_i, i) beats (w_j, j) of every remaining local neighbour; each
+    selected row takes the smallest color its already colored neighbours lack.
+    Selected rows are independent, so they can be colored all at once."""
+    n = lx * ly * lz
+    colors = np.full(n, -1, dtype=np.int32)
+    remaining = np.ones(n, dtype=bool)
+    rng = np.random.default_rng(seed)
+    while remaining.any():
+        w = rng.random(n)
+        sel = np.zeros(n, dtype=bool)
+        for a in range(0, n, chunk):
+            rows = np.arange(a, min(n, a + chunk), dtype=np.int64)
+            nb = _local_neighbours(lx, ly, lz, rows)
+            valid = nb >= 0
+            nbc = np.where(valid, nb, 0)
+            live = valid & remaining[nbc]
+            wi, wj = w[rows][:, None], w[nbc]
+            beats = (wi > wj) | ((wi == wj) & (rows[:, None] > nbc))
+            sel[rows] = remaining[rows] & np.all(beats | ~live, axis=1)
+        idx = np.flatnonzero(sel)
+        for a in range(0, len(idx), chunk):
+            rows = idx[a:a + chunk]
+            nb = _local_neighbours(lx, ly, lz, rows)
+            cn = np.where(nb >= 0, colors[np.where(nb >= 0, nb, 0)], -1)
+            used = np.zeros(len(rows), dtype=np.int64)
+            for s in range(26):
+                c = cn[:, s]
+                used |= np.where(c >= 0, np.left_shift(1, np.maximum(c, 0)), 0)
+            free = ~used
+            colors[rows] = (np.log2((free & -free).astype(np.float64))).astype(np.int32)
+        remaining &= ~sel
+    num_colors = int(colors.max()) + 1 if n else 0
+    counts = np.bincount(colors, minlength=num_colors)
+    offsets = np.zeros(num_colors + 1, dtype=np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    nat = np.arange(n, dtype=np.int64)
+    perm = np.lexsort((nat, colors))
+    iperm = np.empty_like(perm)
+    iperm[perm] = nat
+    return Coloring(color=colors, num_colors=num_colors, color_offsets=offsets, perm=perm, iperm=iperm)
+
+
 def color(A_or_dims, strategy="greedy", seed=0):
-    """Coloring of a level given its local dims (or a domain with ``local_dims``)."""
-    if strategy != "greedy":
-        raise NotImplementedError(
-            f"coloring strategy {strategy!r}: only 'greedy' is built for the device path "
-            "(JPL is SURVEY.md 8(f) F4)")
+    """Coloring of a level given its local dims (or a domain with ``local_dims``)
+    (ref: coloring.py:36-82)."""
     dims = getattr(A_or_dims, "local_dims", A_or_dims)
-    return greedy_coloring(*dims)
+    if strategy == "greedy":
+        return greedy_coloring(*dims)
+    if strategy == "jpl":
+        return jpl_coloring(*dims, seed=seed)
+    raise ValueError(f"unknown coloring strategy: {strategy!r}")

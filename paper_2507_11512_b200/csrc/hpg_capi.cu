@@ -100,7 +100,7 @@ Geom make_geom(const int l[3], const int c[3], const int p[3]) {
     }
     g.off[col + 1] = g.off[col] + size;
   }
-  for (int col = g.ncolors + 1; col < 9; ++col) g.off[col] = g.n;
+  for (int col = g.ncolors + 1; col <= hpg::kMaxColors; ++col) g.off[col] = g.n;
   // neighbours sorted by rank id; halo slots in that order (ref: comm.py:219-227)
   struct Nb {
     int rank, idx;
@@ -150,6 +150,9 @@ struct Level {
   double* v64 = nullptr;
   float* v32 = nullptr;
   int32_t* inj = nullptr;  // (coarse levels) dst[j] for fine color-0 row j
+  int32_t* f2c = nullptr;  // (coarse levels, general colorings) fine row of coarse row i
+  int32_t* perm_d = nullptr;   // general coloring tables (null: greedy closed form)
+  int32_t* iperm_d = nullptr;
   uint8_t* hflag = nullptr;    // rows reading halo slots (multi-rank)
   int32_t* bnd = nullptr;      // all such rows
   int64_t nbnd = 0;
@@ -202,6 +205,7 @@ struct hpg_ctx {
   double* pinned = nullptr;     // 256 host doubles
   int64_t launches = 0;
   bool cgs_fused = true;
+  bool general = false;  // some level uses an explicit (non-greedy) coloring
   bool pdl = true;
   int gs_minb = 3;
   int64_t tail_rows = 0;        // levels with n <= tail_rows run in the persistent tail kernel
@@ -416,8 +420,12 @@ int restrict_(hpg_ctx* c, int l, const T* rf, const T* zf, T* rcoarse) {
   Timed tm(c, M_RESTRICT);
   Level& F = c->lev[l];
   Level& C = c->lev[l + 1];
-  CUDA_TRY(launch_pdl(c, hpg::k_restrict<T>, grid_for(C.n), 256, F.cols, (const T*)vals_of<T>(F), F.ld, C.n,
-                      (const int32_t*)C.inj, rf, zf, rcoarse));
+  if (C.f2c)
+    CUDA_TRY(launch_pdl(c, hpg::k_restrict_gen<T>, grid_for(C.n), 256, F.cols, (const T*)vals_of<T>(F), F.ld, C.n,
+                        (const int32_t*)C.f2c, rf, zf, rcoarse));
+  else
+    CUDA_TRY(launch_pdl(c, hpg::k_restrict<T>, grid_for(C.n), 256, F.cols, (const T*)vals_of<T>(F), F.ld, C.n,
+                        (const int32_t*)C.inj, rf, zf, rcoarse));
   ++c->launches;
   return HPG_OK;
 }
@@ -426,7 +434,10 @@ template <typename T>
 int prolong_(hpg_ctx* c, int l, T* zf, const T* zc) {
   Timed tm(c, M_PROLONG);
   Level& C = c->lev[l + 1];
-  CUDA_TRY(launch_pdl(c, hpg::k_prolong<T>, grid_for(C.n), 256, C.n, (const int32_t*)C.inj, zf, zc));
+  if (C.f2c)
+    CUDA_TRY(launch_pdl(c, hpg::k_prolong_gen<T>, grid_for(C.n), 256, C.n, (const int32_t*)C.f2c, zf, zc));
+  else
+    CUDA_TRY(launch_pdl(c, hpg::k_prolong<T>, grid_for(C.n), 256, C.n, (const int32_t*)C.inj, zf, zc));
   ++c->launches;
   return HPG_OK;
 }
@@ -478,7 +489,7 @@ int vcycle_tail(hpg_ctx* c, int l, const T* r, T* z) {
 // V-cycle with zero initial guess (ref: multigrid.py:140-171)
 template <typename T>
 int vcycle(hpg_ctx* c, int l, const T* r, T* z) {
-  if (c->nranks == 1 && l > 0 && c->lev[l].n <= c->tail_rows && c->nlev - l <= hpg::kMaxTail)
+  if (c->nranks == 1 && l > 0 && c->lev[l].n <= c->tail_rows && c->nlev - l <= hpg::kMaxTail && !c->general)
     return vcycle_tail<T>(c, l, r, z);
   const bool last = l == c->nlev - 1;
   const int sweeps = last ? c->nu_c : c->nu1;
@@ -716,7 +727,7 @@ int gemv_t(hpg_ctx* c, const T* Q, int64_t ldq, int k, const double* y, T* out) 
 void free_level(Level& L) {
   for (void* p : {(void*)L.cols, (void*)L.v64, (void*)L.v32, (void*)L.inj, (void*)L.send_idx, L.send_buf,
                   (void*)L.z64, (void*)L.z32, (void*)L.r64, (void*)L.r32, (void*)L.hflag, (void*)L.bnd,
-                  (void*)L.bnd0})
+                  (void*)L.bnd0, (void*)L.f2c, (void*)L.perm_d, (void*)L.iperm_d})
     if (p) cudaFree(p);
   L = Level();
 }
@@ -727,6 +738,68 @@ int dmalloc(P** p, size_t bytes, size_t* acc) {
   CUDA_TRY(cudaMalloc(&q, std::max<size_t>(bytes, 16)));
   *p = (P*)q;
   if (acc) *acc += bytes;
+  return HPG_OK;
+}
+
+// (Re)build a level's permutation-dependent structure: ELL rows, send lists and
+// the interior/boundary split.  `first` allocates the send/split buffers.
+int build_structure(hpg_ctx* c, Level& L, bool first) {
+  int rc;
+  if (L.n) {
+    hpg::k_build_level<<<grid_for(L.n, 128), 128, 0, c->stream>>>(L.g, L.ld, L.cols, L.v64, L.v32);
+    LAUNCH_CHECK();
+  }
+  // halo plan: one send list per neighbour, in ascending neighbour rank
+  struct Tmp {
+    int rank, idx, sx, sy, sz;
+  };
+  std::vector<Tmp> t;
+  for (int i = 0; i < 27; ++i)
+    if (L.g.nbr_rank[i] >= 0) t.push_back({L.g.nbr_rank[i], i, i % 3 - 1, (i / 3) % 3 - 1, i / 9 - 1});
+  std::sort(t.begin(), t.end(), [](const Tmp& a, const Tmp& b) { return a.rank < b.rank; });
+  if (first) {
+    int64_t off = 0;
+    for (auto& e : t) {
+      const int64_t cnt = hpg::region_size(L.g, e.sx, e.sy, e.sz);
+      L.nbrs.push_back({e.rank, e.idx, off, cnt, L.g.halo_base[e.idx]});
+      off += cnt;
+    }
+    L.send_total = off;
+    if (off) {
+      if ((rc = dmalloc(&L.send_idx, off * 4, &L.bytes))) return rc;
+      if ((rc = dmalloc((char**)&L.send_buf, off * 8, &L.bytes))) return rc;
+    }
+  }
+  for (size_t i = 0; i < t.size(); ++i) {
+    const Nbr& nb = L.nbrs[i];
+    hpg::k_build_send<<<grid_for(nb.cnt), 256, 0, c->stream>>>(L.g, t[i].sx, t[i].sy, t[i].sz, nb.cnt,
+                                                                L.send_idx + nb.send_off);
+    LAUNCH_CHECK();
+  }
+  if (!L.nbrs.empty() && L.n) {
+    // interior / boundary split for the overlapped exchange
+    if (first && (rc = dmalloc(&L.hflag, L.n, &L.bytes))) return rc;
+    hpg::k_build_halo_flags<<<grid_for(L.n), 256, 0, c->stream>>>(L.g, L.hflag);
+    LAUNCH_CHECK();
+    std::vector<uint8_t> f(L.n);
+    CUDA_TRY(cudaMemcpyAsync(f.data(), L.hflag, L.n, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    std::vector<int32_t> all, c0;
+    for (int64_t i = 0; i < L.n; ++i)
+      if (f[i]) {
+        all.push_back((int32_t)i);
+        if (i < L.g.off[1]) c0.push_back((int32_t)i);
+      }
+    L.nbnd = (int64_t)all.size();
+    L.nbnd0 = (int64_t)c0.size();
+    if (L.bnd) cudaFree(L.bnd);
+    if (L.bnd0) cudaFree(L.bnd0);
+    L.bnd = L.bnd0 = nullptr;
+    if ((rc = dmalloc(&L.bnd, std::max<int64_t>(1, L.nbnd) * 4, &L.bytes))) return rc;
+    if ((rc = dmalloc(&L.bnd0, std::max<int64_t>(1, L.nbnd0) * 4, &L.bytes))) return rc;
+    if (L.nbnd) CUDA_TRY(cudaMemcpy(L.bnd, all.data(), L.nbnd * 4, cudaMemcpyHostToDevice));
+    if (L.nbnd0) CUDA_TRY(cudaMemcpy(L.bnd0, c0.data(), L.nbnd0 * 4, cudaMemcpyHostToDevice));
+  }
   return HPG_OK;
 }
 
@@ -745,56 +818,7 @@ int build_level(hpg_ctx* c, Level& L, const int dims[3]) {
   CUDA_TRY(cudaMemsetAsync(L.cols, 0, slots * 4, c->stream));
   CUDA_TRY(cudaMemsetAsync(L.v64, 0, slots * 8, c->stream));
   CUDA_TRY(cudaMemsetAsync(L.v32, 0, slots * 4, c->stream));
-  if (L.n) {
-    hpg::k_build_level<<<grid_for(L.n, 128), 128, 0, c->stream>>>(L.g, L.ld, L.cols, L.v64, L.v32);
-    LAUNCH_CHECK();
-  }
-  // halo plan: one send list per neighbour, in ascending neighbour rank
-  struct Tmp {
-    int rank, idx, sx, sy, sz;
-  };
-  std::vector<Tmp> t;
-  for (int i = 0; i < 27; ++i)
-    if (L.g.nbr_rank[i] >= 0) t.push_back({L.g.nbr_rank[i], i, i % 3 - 1, (i / 3) % 3 - 1, i / 9 - 1});
-  std::sort(t.begin(), t.end(), [](const Tmp& a, const Tmp& b) { return a.rank < b.rank; });
-  int64_t off = 0;
-  for (auto& e : t) {
-    const int64_t cnt = hpg::region_size(L.g, e.sx, e.sy, e.sz);
-    L.nbrs.push_back({e.rank, e.idx, off, cnt, L.g.halo_base[e.idx]});
-    off += cnt;
-  }
-  L.send_total = off;
-  if (off) {
-    if ((rc = dmalloc(&L.send_idx, off * 4, &L.bytes))) return rc;
-    if ((rc = dmalloc((char**)&L.send_buf, off * 8, &L.bytes))) return rc;
-    for (size_t i = 0; i < t.size(); ++i) {
-      const Nbr& nb = L.nbrs[i];
-      hpg::k_build_send<<<grid_for(nb.cnt), 256, 0, c->stream>>>(L.g, t[i].sx, t[i].sy, t[i].sz, nb.cnt,
-                                                                  L.send_idx + nb.send_off);
-      LAUNCH_CHECK();
-    }
-  }
-  if (!L.nbrs.empty() && L.n) {
-    // interior / boundary split for the overlapped exchange
-    if ((rc = dmalloc(&L.hflag, L.n, &L.bytes))) return rc;
-    hpg::k_build_halo_flags<<<grid_for(L.n), 256, 0, c->stream>>>(L.g, L.hflag);
-    LAUNCH_CHECK();
-    std::vector<uint8_t> f(L.n);
-    CUDA_TRY(cudaMemcpyAsync(f.data(), L.hflag, L.n, cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    std::vector<int32_t> all, c0;
-    for (int64_t i = 0; i < L.n; ++i)
-      if (f[i]) {
-        all.push_back((int32_t)i);
-        if (i < L.g.off[1]) c0.push_back((int32_t)i);
-      }
-    L.nbnd = (int64_t)all.size();
-    L.nbnd0 = (int64_t)c0.size();
-    if ((rc = dmalloc(&L.bnd, std::max<int64_t>(1, L.nbnd) * 4, &L.bytes))) return rc;
-    if ((rc = dmalloc(&L.bnd0, std::max<int64_t>(1, L.nbnd0) * 4, &L.bytes))) return rc;
-    if (L.nbnd) CUDA_TRY(cudaMemcpy(L.bnd, all.data(), L.nbnd * 4, cudaMemcpyHostToDevice));
-    if (L.nbnd0) CUDA_TRY(cudaMemcpy(L.bnd0, c0.data(), L.nbnd0 * 4, cudaMemcpyHostToDevice));
-  }
+  if ((rc = build_structure(c, L, true))) return rc;
   if ((rc = dmalloc(&L.z64, L.n_ext * 8, &L.bytes))) return rc;
   if ((rc = dmalloc(&L.z32, L.n_ext * 4, &L.bytes))) return rc;
   if ((rc = dmalloc(&L.r64, L.n * 8, &L.bytes))) return rc;
@@ -1116,8 +1140,50 @@ int hpg_export_f2c(hpg_ctx* c, int l, int64_t* f2c) {
   const Level& C = c->lev[l];
   std::vector<int32_t> dst(C.n);
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (C.f2c) {
+    CUDA_TRY(cudaMemcpy(dst.data(), C.f2c, C.n * 4, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < C.n; ++i) f2c[i] = dst[i];
+    return HPG_OK;
+  }
   CUDA_TRY(cudaMemcpy(dst.data(), C.inj, C.n * 4, cudaMemcpyDeviceToHost));
   for (int64_t j = 0; j < C.n; ++j) f2c[dst[j]] = j;  // fine color-0 row j feeds coarse row dst[j]
+  return HPG_OK;
+}
+
+int hpg_set_coloring(hpg_ctx* c, int l, int ncolors, const int64_t* offsets, const int64_t* perm) {
+  int rc = check_level(c, l);
+  if (rc) return rc;
+  Level& L = c->lev[l];
+  if (ncolors < 1 || ncolors > hpg::kMaxColors) return fail(HPG_E_ARG, "ncolors %d out of [1, 27]", ncolors);
+  if (offsets[0] != 0 || offsets[ncolors] != L.n) return fail(HPG_E_ARG, "color offsets must span [0, n)");
+  for (int k = 0; k < ncolors; ++k)
+    if (offsets[k + 1] < offsets[k]) return fail(HPG_E_ARG, "color offsets must be non-decreasing");
+  std::vector<int32_t> p32(L.n), ip32(L.n, -1);
+  for (int64_t i = 0; i < L.n; ++i) {
+    if (perm[i] < 0 || perm[i] >= L.n || ip32[perm[i]] >= 0) return fail(HPG_E_ARG, "perm is not a permutation");
+    p32[i] = (int32_t)perm[i];
+    ip32[perm[i]] = (int32_t)i;
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (!L.perm_d && (rc = dmalloc(&L.perm_d, std::max<int64_t>(1, L.n) * 4, &L.bytes))) return rc;
+  if (!L.iperm_d && (rc = dmalloc(&L.iperm_d, std::max<int64_t>(1, L.n) * 4, &L.bytes))) return rc;
+  CUDA_TRY(cudaMemcpy(L.perm_d, p32.data(), L.n * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(L.iperm_d, ip32.data(), L.n * 4, cudaMemcpyHostToDevice));
+  L.g.perm_tab = L.perm_d;
+  L.g.iperm_tab = L.iperm_d;
+  L.g.ncolors = ncolors;
+  for (int k = 0; k <= hpg::kMaxColors; ++k) L.g.off[k] = k <= ncolors ? offsets[k] : L.n;
+  c->general = true;
+  if ((rc = build_structure(c, L, false))) return rc;
+  // injection maps of the coarse levels that touch this one
+  for (int cl = std::max(1, l); cl <= std::min(l + 1, c->nlev - 1); ++cl) {
+    Level& C = c->lev[cl];
+    if (!C.f2c && (rc = dmalloc(&C.f2c, std::max<int64_t>(1, C.n) * 4, &C.bytes))) return rc;
+    if (C.n) hpg::k_build_f2c<<<grid_for(C.n), 256, 0, c->stream>>>(C.g, c->lev[cl - 1].g, C.f2c);
+    LAUNCH_CHECK();
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
   return HPG_OK;
 }
 

@@ -29,6 +29,7 @@ namespace hpg {
 
 constexpr int kWidth = 27;
 constexpr int kDiagSlot = 13;  // (0,0,0) in offset order
+constexpr int kMaxColors = 27; // first-fit on a 27-point lattice never needs more
 
 struct Geom {
   int lx, ly, lz;        // local extent
@@ -37,7 +38,12 @@ struct Geom {
   int ncolors;
   int bit[3];            // parity bit of each axis in the color id, -1 if extent < 2
   int64_t n;             // owned rows
-  int64_t off[9];        // color block offsets (ncolors+1 used)
+  int64_t off[kMaxColors + 1];  // color block offsets (ncolors+1 used)
+  // General (e.g. JPL) colorings: explicit tables instead of the greedy closed
+  // form (device pointers; null for greedy).  perm: new row -> natural row,
+  // iperm: natural row -> new row (ref: coloring.py:78-80).
+  const int32_t* perm_tab;
+  const int32_t* iperm_tab;
   int64_t halo_base[27]; // per face/edge/corner (index of offset), -1 if no neighbour
   int64_t halo_size;
   int nbr_rank[27];      // rank id of the neighbour across each face/edge/corner, -1 if none
@@ -55,6 +61,7 @@ HPG_HD int color_of(const Geom& g, int x, int y, int z) {
 
 // natural local coords -> color-permuted row
 HPG_HD int64_t iperm(const Geom& g, int x, int y, int z) {
+  if (g.iperm_tab) return g.iperm_tab[x + (int64_t)g.lx * (y + (int64_t)g.ly * z)];
   const int c = color_of(g, x, y, z);
   const int64_t hx = (g.lx - (x & 1) + 1) >> 1;
   const int64_t hy = (g.ly - (y & 1) + 1) >> 1;
@@ -63,6 +70,13 @@ HPG_HD int64_t iperm(const Geom& g, int x, int y, int z) {
 
 // color-permuted row -> natural local coords
 HPG_HD void decode(const Geom& g, int64_t i, int& x, int& y, int& z) {
+  if (g.perm_tab) {
+    const int64_t nat = g.perm_tab[i];
+    x = (int)(nat % g.lx);
+    y = (int)((nat / g.lx) % g.ly);
+    z = (int)(nat / ((int64_t)g.lx * g.ly));
+    return;
+  }
   int c = 0;
   while (c + 1 < g.ncolors && i >= g.off[c + 1]) ++c;
   const int px = g.bit[0] >= 0 ? (c >> g.bit[0]) & 1 : 0;

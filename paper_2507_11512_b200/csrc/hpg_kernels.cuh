@@ -434,6 +434,42 @@ __global__ void k_build_level(Geom g, int64_t ld, int32_t* __restrict__ cols, do
   }
 }
 
+// General injection (any coloring): f2c[i] = fine row of coarse row i's point
+// (2x, 2y, 2z) (ref: multigrid.py:87-99)
+__global__ void k_build_f2c(Geom gc, Geom gf, int32_t* __restrict__ f2c) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= gc.n) return;
+  int x, y, z;
+  decode(gc, i, x, y, z);
+  f2c[i] = (int32_t)iperm(gf, 2 * x, 2 * y, 2 * z);
+}
+
+// rc[i] = r[f2c[i]] - (A z)[f2c[i]] for any coloring (rows gathered; ref: multigrid.py:107-128)
+template <typename T>
+__global__ void __launch_bounds__(256, 2) k_restrict_gen(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+                                                         int64_t ld, int64_t nc, const int32_t* __restrict__ f2c,
+                                                         const T* __restrict__ r, const T* __restrict__ z,
+                                                         T* __restrict__ rc) {
+  pdl_trigger();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  const int64_t f = f2c[i];
+  T dd;
+  const T acc = row_accumulate<T, false, false, true>(cols, vals, ld, f, z, &dd);
+  rc[i] = sub_rn(r[f], acc);
+}
+
+// z[f2c[i]] += zc[i] for any coloring (ref: multigrid.py:131-137)
+template <typename T>
+__global__ void k_prolong_gen(int64_t nc, const int32_t* __restrict__ f2c, T* __restrict__ z, const T* __restrict__ zc) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  const int64_t f = f2c[i];
+  z[f] = add_rn(z[f], zc[i]);
+}
+
 // dst[j] = coarse iperm of coarse natural index j   (f2c inverse on color-0 rows)
 __global__ void k_build_inject(Geom gc, int32_t* __restrict__ dst) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -122,19 +122,32 @@ def build_hierarchy(domain, levels, world=None, rank=0, strategy="greedy", seed=
     import torch
     if levels < 1:
         raise ValueError("need at least one level")
-    if strategy != "greedy":
-        color_rows(domain, strategy)  # raises NotImplementedError with the reason
+    if strategy not in ("greedy", "jpl"):
+        raise ValueError(f"unknown coloring strategy: {strategy!r}")
     sweeps = sweeps or SmootherWorkspace()
     doms = [domain]
     for _ in range(levels - 1):
         doms.append(doms[-1].coarsen())  # CoarseningError, like the reference
     ctx = Context(domain, levels, sweeps.nu1, sweeps.nu2, sweeps.nu_c, world)
+    colorings = [None] * levels
+    if strategy == "jpl":
+        # host JPL per level (same RNG stream as the reference), then the device
+        # rebuilds each level in that order (ref: multigrid.py:66-70)
+        import ctypes as C
+        for lev, dom in enumerate(doms):
+            col = color_rows(dom, "jpl", seed)
+            colorings[lev] = col
+            offs = np.ascontiguousarray(col.color_offsets, dtype=np.int64)
+            perm = np.ascontiguousarray(col.perm, dtype=np.int64)
+            i64 = C.POINTER(C.c_int64)
+            ctx.call("hpg_set_coloring", lev, col.num_colors, offs.ctypes.data_as(i64),
+                     perm.ctypes.data_as(i64))
     out = []
     for lev, dom in enumerate(doms):
         A = EllMatrix(ctx, lev, _lib.F64)
         A_lo = EllMatrix(ctx, lev, _lib.F32)
         A.domain = A_lo.domain = dom
-        lv = MgLevel(domain=dom, A_hi=A, A_lo=A_lo)
+        lv = MgLevel(domain=dom, A_hi=A, A_lo=A_lo, coloring=colorings[lev])
         lv.plan = HaloPlan(ctx, lev, dom) if world is not None else None
         ne, n = A.n_cols_extended, A.n_rows
         dev = ctx.device

@@ -257,6 +257,45 @@ def make_solves():
         json.dump(out, f, indent=1, sort_keys=True)
 
 
+def make_jpl():
+    """JPL colorings (ref: coloring.py:56-70) and a JPL hierarchy's V-cycle/solve."""
+    _import_ref()
+    from mxpbench.geometry import GlobalProblem
+    from mxpbench.multigrid import build_hierarchy
+    from mxpbench.problem import generate_matrix
+    from mxpbench.coloring import color
+    out = {}
+    for (lx, ly, lz, seed) in [(4, 4, 4, 0), (6, 4, 8, 3), (8, 8, 8, 11), (5, 3, 4, 7), (16, 16, 16, 0)]:
+        A = generate_matrix(GlobalProblem.from_local(lx, ly, lz, 1).domain(0))
+        c = color(A, "jpl", seed=seed)
+        key = f"{lx}x{ly}x{lz}_s{seed}"
+        out[f"color_{key}"] = c.color
+        out[f"perm_{key}"] = c.perm
+        out[f"offsets_{key}"] = c.color_offsets
+    # 16^3, 4 levels, jpl seed 0: level arrays, f2c, a V-cycle on random data
+    h = build_hierarchy(GlobalProblem.from_local(16, 16, 16, 1).domain(0), 4, strategy="jpl", seed=0)
+    rng = np.random.default_rng(5)
+    for li, lv in enumerate(h.levels):
+        out[f"h_l{li}_col_idx"] = lv.A_hi.col_idx
+        out[f"h_l{li}_perm"] = lv.coloring.perm
+        out[f"h_l{li}_offsets"] = lv.coloring.color_offsets
+        if lv.f2c is not None:
+            out[f"h_l{li}_f2c"] = lv.f2c
+    for dt, tag in ((np.float64, "f64"), (np.float32, "f32")):
+        r = rng.standard_normal(h.levels[0].A_hi.n_rows).astype(dt)
+        out[f"h_r_{tag}"] = r
+        out[f"h_vcycle_{tag}"] = h.apply(r.copy()).copy()
+    from mxpbench.krylov import gmres_solve
+    lv = h.levels[0]
+    b = lv.A_hi.values.sum(axis=1)
+    for mode in ("double", "mixed"):
+        res = gmres_solve(lv.A_hi, lv.A_lo, lambda v: h.apply(v), b, x0=np.zeros(lv.A_hi.n_rows),
+                          mode=mode, tol=1e-9, max_iters=300, m=30)
+        out[f"h_solve_{mode}"] = np.array([res.iterations, res.relres])
+    np.savez_compressed(os.path.join(HERE, "jpl.npz"), **out)
+    print("jpl")
+
+
 def make_validation():
     _import_ref()
     from mxpbench.bench import BenchConfig, run_validation
@@ -285,7 +324,7 @@ if __name__ == "__main__":
             r["_xpath"] = path
         print(json.dumps(res))
         sys.exit(0)
-    what = sys.argv[1:] or ["structure", "kernels", "solves", "validation"]
+    what = sys.argv[1:] or ["structure", "kernels", "solves", "validation", "jpl"]
     if "structure" in what:
         make_structure()
     if "kernels" in what:
@@ -294,3 +333,5 @@ if __name__ == "__main__":
         make_solves()
     if "validation" in what:
         make_validation()
+    if "jpl" in what:
+        make_jpl()

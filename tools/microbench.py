@@ -56,6 +56,15 @@ def main():
     us = timeit(lambda: ctx.call("hpg_gs_sweep", 0, _lib.F32, _lib.ptr(r32), _lib.ptr(z32), 0))
     out["gs_sweep_L0_f32_us"] = us
     out["gs_sweep_L0_f32_GBs"] = (nnz * 8 + 3 * n * 4) / us / 1e3
+    z64 = torch.zeros(ne, device="cuda", dtype=torch.float64)
+    r64b = torch.randn(n, device="cuda", dtype=torch.float64)
+    us = timeit(lambda: ctx.call("hpg_gs_sweep", 0, _lib.F64, _lib.ptr(r64b), _lib.ptr(z64), 0))
+    out["gs_sweep_L0_f64_us"] = us
+    out["gs_sweep_L0_f64_GBs"] = (nnz * 12 + 3 * n * 8) / us / 1e3
+    y64 = torch.empty(n, device="cuda", dtype=torch.float64)
+    us = timeit(lambda: ctx.call("hpg_spmv", 0, _lib.F64, _lib.ptr(x64), _lib.ptr(y64)))
+    out["spmv_f64_us"] = us
+    out["spmv_f64_GBs"] = (nnz * 12 + 2 * n * 8) / us / 1e3
     us = timeit(lambda: hier.apply(r32, out=z32))
     out["vcycle_f32_us"] = us
     us = timeit(lambda: hier.apply(r64 if False else b64, out=x64))
