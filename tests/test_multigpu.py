@@ -21,10 +21,12 @@ def _gpus():
         return 0
 
 
-def _run(nproc, L, levels):
+def _run(nproc, L, levels, env=None):
+    e = dict(os.environ)
+    e.update(env or {})
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--local-addr", "127.0.0.1",
            "--nproc-per-node", str(nproc), os.path.join(ROOT, "tools", "mgpu_check.py"), str(L), str(levels)]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=e)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     line = [x for x in p.stdout.splitlines() if x.startswith("{")][-1]
     return json.loads(line)
@@ -45,6 +47,18 @@ def test_two_ranks_16():
     assert out["validation"]["mode"] == "fullscale" and out["validation"]["n_d"] == 23
     assert min(env) - ncyc <= out["validation"]["n_ir"] <= max(env) + ncyc
     assert out["summary"]["raw_gflops"] > 0
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("env", [{"HPG_P2P": "0"}, {"HPG_OVERLAP": "1"}, {"HPG_P2P": "0", "HPG_OVERLAP": "1"},
+                                 {"HPG_CGS_FUSED": "0"}])
+def test_two_ranks_alternative_paths(env):
+    """NCCL data path, overlapped exchange and per-pass CGS2: same bitwise kernels,
+    same fp64 count as the reference (23)."""
+    out = _run(2, 8, 3, env)
+    for rk in out["checks"]:
+        assert all(rk.values()), (env, out["checks"])
+    assert out["solves"]["double"]["converged"] and out["solves"]["mixed"]["relres"] < 1e-9
 
 
 @pytest.mark.skipif(_gpus() < 4, reason="needs 4 GPUs")
