@@ -335,3 +335,9 @@ if __name__ == "__main__":
         make_validation()
     if "jpl" in what:
         make_jpl()
+# MatrixMarket fixtures (tests/golden/mtx_sha256.json) were produced with:
+#   from mxpbench.bench import BenchConfig, dump_matrix
+#   dump_matrix(BenchConfig(local_nx=8, local_ny=8, local_nz=8), path)              -> "l8r1"
+#   dump_matrix(BenchConfig(local_nx=4, ..., ranks=2, mg_levels=2), path)            -> "l4r2"
+#   dump_matrix(BenchConfig(local_nx=4, ..., ranks=8, mg_levels=2), path)            -> "l4r8"
+# and hashed with hashlib.sha256 over the file bytes.

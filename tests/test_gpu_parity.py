@@ -264,3 +264,17 @@ def test_jpl_hierarchy_and_vcycle_bitwise_vs_reference():
     assert rd.iterations == int(ref_d[0]) and rd.relres == pytest.approx(ref_d[1], rel=1e-6)
     assert rm.converged and abs(rm.iterations - int(ref_m[0])) <= 2
     h.close()
+
+
+def test_run_benchmark_is_deterministic():
+    # ref: tests/test_bench.py:148-154 -- two runs agree except for timings
+    from paper_2507_11512_b200.bench import BenchConfig, run_benchmark
+    cfg = BenchConfig(local_nx=8, local_ny=8, local_nz=8, time_seconds=0)
+
+    def strip(rep):
+        out = {k: v for k, v in rep.items() if k not in ("mxp", "double", "summary")}
+        for phase in ("mxp", "double"):
+            out[phase] = {m: rep[phase][m]["flops"] for m in rep[phase]}
+        return out
+
+    assert strip(run_benchmark(cfg)) == strip(run_benchmark(cfg))
