@@ -155,7 +155,8 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
  *   "pdl"        1: stencil kernels use programmatic dependent launch
  *   "overlap"    1: multi-rank SpMV / GS overlap the halo exchange with interior rows
  *   "overlap_rows" only levels with at least this many rows overlap (default 2^20)
- *   "p2p"        1: NVLink peer-memory halo exchange + all-reduce (after hpg_p2p_open) */
+ *   "p2p"        1: NVLink peer-memory halo exchange + all-reduce (after hpg_p2p_open)
+ *   "graphs"     1: single-rank V-cycles replay a captured CUDA graph per (prec, r, z) */
 int hpg_set_option(hpg_ctx* ctx, const char* key, int64_t value);
 
 /* NVLink peer memory (csrc/hpg_p2p.cuh).  Collective setup, nranks > 1:

@@ -172,6 +172,18 @@ struct Level {
 
 }  // namespace
 
+struct GraphKey {
+  int prec;
+  const void* r;
+  const void* z;
+  bool operator==(const GraphKey& o) const { return prec == o.prec && r == o.r && z == o.z; }
+};
+struct GraphEntry {
+  GraphKey key;
+  cudaGraphExec_t exec;
+  uint64_t stamp;
+};
+
 struct hpg_ctx {
   int device = 0, rank = 0, nranks = 1;
   int procs[3] = {1, 1, 1}, coords[3] = {0, 0, 0};
@@ -206,6 +218,9 @@ struct hpg_ctx {
   int64_t launches = 0;
   bool cgs_fused = true;
   bool general = false;  // some level uses an explicit (non-greedy) coloring
+  bool graphs = true;    // replay captured V-cycles (single rank)
+  std::vector<GraphEntry> gcache;
+  uint64_t gclock = 0;
   bool pdl = true;
   int gs_minb = 3;
   int64_t tail_rows = 0;        // levels with n <= tail_rows run in the persistent tail kernel
@@ -1027,6 +1042,8 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     c->cgs_fused = !(f && f[0] == '0');
     const char* mb = getenv("HPG_GS_MINB");
     if (mb) c->gs_minb = atoi(mb);
+    const char* gr = getenv("HPG_GRAPHS");
+    if (gr) c->graphs = gr[0] != '0';
     const char* pp = getenv("HPG_P2P");
     if (pp) c->p2p_want = pp[0] != '0';
     const char* ov = getenv("HPG_OVERLAP");
@@ -1076,6 +1093,7 @@ int hpg_destroy(hpg_ctx* c) {
   if (c->sym) cudaFree(c->sym);
   if (c->d_peer) cudaFree(c->d_peer);
   if (c->done) cudaFree(c->done);
+  for (auto& e : c->gcache) cudaGraphExecDestroy(e.exec);
   for (auto e : c->events) cudaEventDestroy(e);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
@@ -1226,6 +1244,41 @@ int hpg_prolong(hpg_ctx* c, int l, int prec, void* zf, const void* zc) {
 int hpg_vcycle(hpg_ctx* c, int prec, const void* r, void* z) {
   int rc = check_level(c, 0);
   if (rc || (rc = check_prec(prec))) return rc;
+  // Single rank, no motif timers: replay a CUDA graph of the whole V-cycle
+  // (~60 dependent launches) captured once per (precision, r, z).
+  if (c->graphs && c->nranks == 1 && !c->timing) {
+    const GraphKey key{prec, r, z};
+    for (auto& e : c->gcache)
+      if (e.key == key) {
+        e.stamp = ++c->gclock;
+        CUDA_TRY(cudaGraphLaunch(e.exec, c->stream));
+        return HPG_OK;
+      }
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    rc = prec == HPG_F64 ? vcycle<double>(c, 0, (const double*)r, (double*)z)
+                         : vcycle<float>(c, 0, (const float*)r, (float*)z);
+    cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess) return fail(HPG_E_CUDA, "V-cycle capture: %s", cudaGetErrorString(ce));
+    cudaGraphExec_t exec = nullptr;
+    ce = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return fail(HPG_E_CUDA, "V-cycle instantiate: %s", cudaGetErrorString(ce));
+    if (c->gcache.size() >= 96) {  // evict the least recently used
+      size_t lru = 0;
+      for (size_t q = 1; q < c->gcache.size(); ++q)
+        if (c->gcache[q].stamp < c->gcache[lru].stamp) lru = q;
+      cudaGraphExecDestroy(c->gcache[lru].exec);
+      c->gcache.erase(c->gcache.begin() + lru);
+    }
+    c->gcache.push_back({key, exec, ++c->gclock});
+    CUDA_TRY(cudaGraphLaunch(exec, c->stream));
+    return HPG_OK;
+  }
   return prec == HPG_F64 ? vcycle<double>(c, 0, (const double*)r, (double*)z)
                          : vcycle<float>(c, 0, (const float*)r, (float*)z);
 }
@@ -1427,6 +1480,11 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   else if (!strcmp(key, "p2p")) c->p2p = value != 0 && !c->peer_sym.empty();
   else if (!strcmp(key, "overlap_rows")) c->overlap_rows = value;
   else if (!strcmp(key, "gs_minb")) c->gs_minb = (int)value;
+  else if (!strcmp(key, "graphs")) {
+    c->graphs = value != 0;
+    for (auto& e : c->gcache) cudaGraphExecDestroy(e.exec);
+    c->gcache.clear();
+  }
   else if (!strcmp(key, "tail_rows")) c->tail_rows = value;
   else return fail(HPG_E_ARG, "unknown option %s", key);
   return HPG_OK;
