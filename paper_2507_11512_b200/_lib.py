@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhpgmxp.so")
+# HPG_LIB: load another build of the same sources (A/B experiments)
+LIB_PATH = os.environ.get("HPG_LIB") or os.path.join(HERE, "libhpgmxp.so")
 
 F64 = 0
 F32 = 1
