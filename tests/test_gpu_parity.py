@@ -278,3 +278,50 @@ def test_run_benchmark_is_deterministic():
         return out
 
     assert strip(run_benchmark(cfg)) == strip(run_benchmark(cfg))
+
+
+@pytest.mark.parametrize("dims", [(16, 8, 32), (24, 16, 8), (8, 8, 8)])
+def test_nonuniform_boxes_vcycle_bitwise_vs_oracle(dims):
+    """Non-cubic local boxes (x, y, z extents differ) through the whole V-cycle."""
+    import hpgmxp_oracle as O
+    from paper_2507_11512_b200.geometry import GlobalProblem
+    from paper_2507_11512_b200.multigrid import build_hierarchy
+    levels = 3 if min(dims) >= 8 else 2
+    h = build_hierarchy(GlobalProblem.from_local(*dims, 1).domain(0), levels)
+    s = O.Solver(*dims, 1, levels)
+    rng = np.random.default_rng(sum(dims))
+    for dt, tdt in ((np.float64, torch.float64), (np.float32, torch.float32)):
+        r = rng.standard_normal(h.levels[0].A_hi.n_rows).astype(dt)
+        np.testing.assert_array_equal(h.apply(_dev(r, tdt)).cpu().numpy(), s.vcycle([r])[0])
+    h.close()
+
+
+def test_execution_variants_agree_bitwise():
+    """Tuning switches never change results: the persistent V-cycle tail kernel,
+    CUDA-graph replay and PDL give the same V-cycle bits; the host-pipelined and
+    plain Arnoldi loops give the same iterations and solution."""
+    import os
+    from paper_2507_11512_b200.krylov import gmres_solve
+    from paper_2507_11512_b200.problem import generate_rhs
+    h = _hier(32)
+    ctx = h.ctx
+    r = torch.randn(h.levels[0].A_hi.n_rows, device="cuda", generator=torch.Generator("cuda").manual_seed(3))
+    ref = h.apply(r).cpu().numpy()
+    for key, val in (("tail_rows", 1 << 30), ("graphs", 0), ("pdl", 0)):
+        ctx.set_option(key, val)
+        np.testing.assert_array_equal(h.apply(r).cpu().numpy(), ref)
+    ctx.set_option("tail_rows", 0)
+    ctx.set_option("graphs", 1)
+    ctx.set_option("pdl", 1)
+    lv = h.levels[0]
+    b = generate_rhs(lv.A_hi).b
+    outs = []
+    for pipe in ("1", "0"):
+        os.environ["HPG_PIPELINE"] = pipe
+        x = np.zeros(lv.A_hi.n_rows)
+        res = gmres_solve(lv.A_hi, lv.A_lo, h.preconditioner(), b, x0=x, mode="mixed")
+        outs.append((res.iterations, res.relres, x))
+    os.environ.pop("HPG_PIPELINE")
+    assert outs[0][0] == outs[1][0] and outs[0][1] == outs[1][1]
+    np.testing.assert_array_equal(outs[0][2], outs[1][2])
+    h.close()
