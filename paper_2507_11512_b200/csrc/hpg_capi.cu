@@ -286,20 +286,28 @@ cudaError_t launch_pdl(hpg_ctx* c, void (*k)(KArgs...), int grid, int block, Arg
   return cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...);
 }
 
+// one kernel: P2P pack into the neighbours' staging, publish, wait, unpack
+int halo_p2p(hpg_ctx* c, int l, int prec, void* v, cudaStream_t st) {
+  Level& L = c->lev[l];
+  const uint64_t seq = ++c->halo_seq;
+  const int grid = (int)std::min<int64_t>(296, std::max<int64_t>(1, cdiv(L.p2p.total, 256 * 8)));
+  cudaStream_t keep = c->stream;
+  c->stream = st;  // launch_pdl enqueues on c->stream
+  cudaError_t e = prec == HPG_F64
+                      ? launch_pdl(c, hpg::k_halo_p2p<double>, grid, 256, (double*)v, (const int32_t*)L.send_idx,
+                                   L.p2p, seq, c->done)
+                      : launch_pdl(c, hpg::k_halo_p2p<float>, grid, 256, (float*)v, (const int32_t*)L.send_idx,
+                                   L.p2p, seq, c->done);
+  c->stream = keep;
+  if (e != cudaSuccess) return fail(HPG_E_CUDA, "halo kernel launch: %s", cudaGetErrorString(e));
+  ++c->launches;
+  return HPG_OK;
+}
+
 int do_exchange(hpg_ctx* c, int l, int prec, void* v) {
   Level& L = c->lev[l];
   if (c->nranks == 1 || L.nbrs.empty()) return HPG_OK;
-  if (c->p2p) {  // one kernel: P2P pack into the neighbours' staging, publish, wait, unpack
-    const uint64_t seq = ++c->halo_seq;
-    const int grid = (int)std::min<int64_t>(296, std::max<int64_t>(1, cdiv(L.p2p.total, 256 * 4)));
-    if (prec == HPG_F64)
-      hpg::k_halo_p2p<double><<<grid, 256, 0, c->stream>>>((double*)v, L.send_idx, L.p2p, seq, c->done);
-    else
-      hpg::k_halo_p2p<float><<<grid, 256, 0, c->stream>>>((float*)v, L.send_idx, L.p2p, seq, c->done);
-    LAUNCH_CHECK();
-    ++c->launches;
-    return HPG_OK;
-  }
+  if (c->p2p) return halo_p2p(c, l, prec, v, c->stream);
   if (L.send_total) {
     if (prec == HPG_F64)
       hpg::k_pack<double><<<grid_for(L.send_total), 256, 0, c->stream>>>((const double*)v, L.send_idx, L.send_total,
@@ -327,6 +335,12 @@ int exchange_begin(hpg_ctx* c, int l, int prec, void* v) {
   Level& L = c->lev[l];
   CUDA_TRY(cudaEventRecord(c->ev_ready, c->stream));
   CUDA_TRY(cudaStreamWaitEvent(c->halo, c->ev_ready, 0));
+  if (c->p2p) {
+    int rc = halo_p2p(c, l, prec, v, c->halo);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(c->ev_done, c->halo));
+    return HPG_OK;
+  }
   if (L.send_total) {
     if (prec == HPG_F64)
       hpg::k_pack<double><<<grid_for(L.send_total), 256, 0, c->halo>>>((const double*)v, L.send_idx, L.send_total,

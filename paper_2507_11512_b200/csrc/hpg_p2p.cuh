@@ -44,7 +44,16 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   return v;
 }
 __device__ __forceinline__ void spin_until(const uint64_t* p, uint64_t seq) {
-  while (ld_acquire_sys(p) < seq) __nanosleep(64);
+  while (ld_acquire_sys(p) < seq) {
+  }
+}
+// Make every store of this CTA so far visible system-wide before the caller's
+// next store: the CTA barrier orders the other threads' stores before thread
+// 0's system-scope fence, which is cumulative (one fence per CTA, not per thread).
+__device__ __forceinline__ void cta_fence_sys() {
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  __syncthreads();
 }
 
 struct P2PAr {
@@ -66,8 +75,7 @@ __device__ void p2p_allreduce_block(T* buf, int cnt, const P2PAr& ar, uint64_t s
       slot[threadIdx.x] = v;
     }
   }
-  __threadfence_system();
-  __syncthreads();
+  cta_fence_sys();
   if (threadIdx.x == 0) {
     for (int q = 0; q < ar.nranks; ++q)
       if (q != ar.me) st_release_sys((uint64_t*)(ar.peer[q] + kSymArFlags) + ar.me, seq);
@@ -115,6 +123,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_halo_p2p(T* v, const int32_t* __restrict__ send_idx,
                                                   const __grid_constant__ P2PHalo h, uint64_t seq,
                                                   unsigned int* done) {
+  // launched with PDL: wait for the producer of v before packing it
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int par = (int)(seq & 1);
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gs = (int64_t)gridDim.x * blockDim.x;
@@ -124,8 +134,7 @@ __global__ void __launch_bounds__(256) k_halo_p2p(T* v, const int32_t* __restric
     T* dst = (T*)nb.remote_stage + par * nb.cnt;
     for (int64_t e = gt; e < nb.cnt; e += gs) dst[e] = v[send_idx[nb.send_off + e]];
   }
-  __threadfence_system();
-  __syncthreads();
+  cta_fence_sys();
   __shared__ bool last;
   if (threadIdx.x == 0) {
     const unsigned int prev = atomicAdd(done, 1u);
