@@ -374,12 +374,38 @@ class World:
 # stencil kernels (ref: krylov.py:76-107, smoother.py:62-114, multigrid.py:102-137)
 # ----------------------------------------------------------------------------
 
+_POOL = None
+_THREADS = 1
+
+
+def set_threads(k):
+    """Split the row loops over k host threads (numpy releases the GIL in the
+    gathers and ufuncs).  Per-row arithmetic is unchanged, so results are
+    bitwise identical for any k; used for the CPU baseline timing."""
+    global _POOL, _THREADS
+    from concurrent.futures import ThreadPoolExecutor
+    _THREADS = max(1, int(k))
+    _POOL = ThreadPoolExecutor(_THREADS) if _THREADS > 1 else None
+
+
+def _rows_parallel(fn, nrows):
+    """fn(a, b) over row chunks; results concatenated in row order."""
+    if _POOL is None or nrows < 4096 * _THREADS:
+        return fn(0, nrows)
+    cuts = [nrows * t // _THREADS for t in range(_THREADS + 1)]
+    parts = list(_POOL.map(lambda t: fn(cuts[t], cuts[t + 1]), range(_THREADS)))
+    return np.concatenate(parts)
+
+
 def row_products(vals, cols, x):
     """sum_s vals[:, s] * x[cols[:, s]], slot by slot, separate mul and add."""
-    acc = np.zeros(vals.shape[0], dtype=x.dtype)
-    for s in range(vals.shape[1]):
-        acc += vals[:, s] * x[cols[:, s]]
-    return acc
+    def part(a, b):
+        acc = np.zeros(b - a, dtype=x.dtype)
+        v, c = vals[a:b], cols[a:b]
+        for s in range(vals.shape[1]):
+            acc += v[:, s] * x[c[:, s]]
+        return acc
+    return _rows_parallel(part, vals.shape[0])
 
 
 def spmv_rank(lv, x):

@@ -159,3 +159,16 @@ def test_validation_standard_small():
     v = O.run_validation(4, 4, 4, 1, 3)
     assert v["n_d"] == 6 and v["n_ir"] in (7, 8, 9)
     assert v["residual"] == pytest.approx(8.99325262264748e-12, rel=1e-6)
+
+
+def test_threaded_oracle_is_bitwise_identical():
+    """The CPU-baseline timing splits row loops over threads: same bits."""
+    s = O.Solver(16, 16, 16, 1, 4)
+    r = np.random.default_rng(3).standard_normal(4096)
+    a = s.vcycle([r.copy()])[0]
+    O.set_threads(4)
+    try:
+        b = s.vcycle([r.copy()])[0]
+    finally:
+        O.set_threads(1)
+    np.testing.assert_array_equal(a, b)
