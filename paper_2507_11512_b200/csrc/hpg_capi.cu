@@ -219,6 +219,7 @@ struct hpg_ctx {
   bool cgs_fused = true;
   bool general = false;  // some level uses an explicit (non-greedy) coloring
   bool graphs = true;    // replay captured V-cycles (single rank)
+  bool known_zero = true;  // zero sweeps skip loads of known zeros (same arithmetic)
   std::vector<GraphEntry> gcache;
   uint64_t gclock = 0;
   bool pdl = true;
@@ -398,17 +399,20 @@ int allreduce_scal(hpg_ctx* c, T* buf, int cnt) {
 
 template <typename T>
 int gs_pass_launch(hpg_ctx* c, Level& L, int64_t a, int64_t cnt, const T* r, T* z, const uint8_t* skip,
-                   const int32_t* list) {
+                   const int32_t* list, int64_t known0 = -1) {
   const T* vals = vals_of<T>(L);
   if (skip || list)
     CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3, true>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip,
-                        list));
+                        list, known0));
   else if (c->gs_minb == 3)
-    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list));
+    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
+                        known0));
   else if (c->gs_minb == 4)
-    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 4>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list));
+    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 4>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
+                        known0));
   else
-    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 2>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list));
+    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 2>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
+                        known0));
   ++c->launches;
   return HPG_OK;
 }
@@ -423,6 +427,18 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
   Level& L = c->lev[l];
   const int prec = sizeof(T) == 8 ? HPG_F64 : HPG_F32;
   int first = 0, rc;
+  if (zero && c->known_zero) {
+    // zero initial guess (ref: smoother.py:95-96): only the halo tail is cleared;
+    // every owned row is written by its color pass, which forms v * 0 for the
+    // colors not yet updated instead of loading zeros (same arithmetic)
+    if (L.n_ext > L.n)
+      CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n_ext - L.n, 4)), 256, z + L.n, L.n_ext - L.n));
+    for (int col = 0; col < L.g.ncolors; ++col) {
+      const int64_t a = L.g.off[col], b = L.g.off[col + 1];
+      if (b > a && (rc = gs_pass_launch<T>(c, L, a, b - a, r, z, nullptr, nullptr, a))) return rc;
+    }
+    return HPG_OK;
+  }
   if (zero) {
     CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n_ext, 4)), 256, z, L.n_ext));
     ++c->launches;
@@ -1056,6 +1072,8 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     c->cgs_fused = !(f && f[0] == '0');
     const char* mb = getenv("HPG_GS_MINB");
     if (mb) c->gs_minb = atoi(mb);
+    const char* kz = getenv("HPG_KNOWN_ZERO");
+    if (kz) c->known_zero = kz[0] != '0';
     const char* gr = getenv("HPG_GRAPHS");
     if (gr) c->graphs = gr[0] != '0';
     const char* pp = getenv("HPG_P2P");
@@ -1494,6 +1512,7 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   else if (!strcmp(key, "p2p")) c->p2p = value != 0 && !c->peer_sym.empty();
   else if (!strcmp(key, "overlap_rows")) c->overlap_rows = value;
   else if (!strcmp(key, "gs_minb")) c->gs_minb = (int)value;
+  else if (!strcmp(key, "known_zero")) c->known_zero = value != 0;
   else if (!strcmp(key, "graphs")) {
     c->graphs = value != 0;
     for (auto& e : c->gcache) cudaGraphExecDestroy(e.exec);

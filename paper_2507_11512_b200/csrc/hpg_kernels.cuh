@@ -96,9 +96,13 @@ __device__ __forceinline__ T ldv(const T* p) {
   return *p;
 }
 
+// known0 >= 0: columns >= known0 are known to hold 0 (the smoother's zero
+// initial guess for colors not yet updated in this sweep, and the zeroed halo):
+// their products are still formed -- v * 0, the reference's arithmetic -- only
+// the load of a known zero is skipped.
 template <typename T, bool ZERO_DIAG, bool COHERENT = false, bool PDL = false>
 __device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, const T* __restrict__ vals,
-                                            int64_t ld, int64_t i, const T* x, T* d) {
+                                            int64_t ld, int64_t i, const T* x, T* d, int64_t known0 = -1) {
   int32_t c[27];
   T v[27];
 #pragma unroll
@@ -110,7 +114,10 @@ __device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, co
   if (PDL) pdl_wait();  // x may be written by the predecessor kernel
   T g[27];
 #pragma unroll
-  for (int s = 0; s < 27; ++s) g[s] = ldv<COHERENT>(x + (c[s] < 0 ? ~c[s] : c[s]));
+  for (int s = 0; s < 27; ++s) {
+    const int32_t cc = c[s] < 0 ? ~c[s] : c[s];
+    g[s] = (known0 >= 0 && cc >= known0) ? T(0) : ldv<COHERENT>(x + cc);
+  }
   T acc = T(0);
 #pragma unroll
   for (int s = 0; s < 27; ++s) {
@@ -173,9 +180,9 @@ __global__ void __launch_bounds__(256, 2) k_spmv(const int32_t* __restrict__ col
 //   z_i = (r_i - sum_{s != diag} A[i,s] z[col]) / a_ii
 template <typename T, bool COHERENT = false, bool PDL = false>
 __device__ __forceinline__ void gs_row(const int32_t* __restrict__ cols, const T* __restrict__ vals, int64_t ld,
-                                       int64_t i, const T* __restrict__ r, T* z) {
+                                       int64_t i, const T* __restrict__ r, T* z, int64_t known0 = -1) {
   T d = T(0);
-  const T acc = row_accumulate<T, true, COHERENT, PDL>(cols, vals, ld, i, z, &d);
+  const T acc = row_accumulate<T, true, COHERENT, PDL>(cols, vals, ld, i, z, &d, known0);
   z[i] = div_rn(sub_rn(ldv<COHERENT>(r + i), acc), d);
 }
 
@@ -187,7 +194,7 @@ __global__ void __launch_bounds__(256, MINB) k_gs_pass(const int32_t* __restrict
                                                     int64_t ld, int64_t row0, int64_t nrows,
                                                     const T* __restrict__ r, T* z,
                                                     const uint8_t* __restrict__ skip,
-                                                    const int32_t* __restrict__ list) {
+                                                    const int32_t* __restrict__ list, int64_t known0) {
   pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nrows) return;
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(256, MINB) k_gs_pass(const int32_t* __restrict
     if (list) i = list[t];
     if (skip && skip[i]) return;
   }
-  gs_row<T, false, true>(cols, vals, ld, i, r, z);
+  gs_row<T, false, true>(cols, vals, ld, i, r, z, known0);
 }
 
 // Fused residual + injection: for fine color-0 row j < nc,

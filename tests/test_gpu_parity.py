@@ -307,9 +307,10 @@ def test_execution_variants_agree_bitwise():
     ctx = h.ctx
     r = torch.randn(h.levels[0].A_hi.n_rows, device="cuda", generator=torch.Generator("cuda").manual_seed(3))
     ref = h.apply(r).cpu().numpy()
-    for key, val in (("tail_rows", 1 << 30), ("graphs", 0), ("pdl", 0)):
+    for key, val in (("tail_rows", 1 << 30), ("graphs", 0), ("pdl", 0), ("known_zero", 0)):
         ctx.set_option(key, val)
         np.testing.assert_array_equal(h.apply(r).cpu().numpy(), ref)
+    ctx.set_option("known_zero", 1)
     ctx.set_option("tail_rows", 0)
     ctx.set_option("graphs", 1)
     ctx.set_option("pdl", 1)
