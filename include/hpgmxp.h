@@ -156,7 +156,11 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
  *   "overlap"    1: multi-rank SpMV / GS overlap the halo exchange with interior rows
  *   "overlap_rows" only levels with at least this many rows overlap (default 2^20)
  *   "p2p"        1: NVLink peer-memory halo exchange + all-reduce (after hpg_p2p_open)
- *   "graphs"     1: single-rank V-cycles replay a captured CUDA graph per (prec, r, z) */
+ *   "graphs"     1: single-rank V-cycles replay a captured CUDA graph per (prec, r, z)
+ *   "known_zero" 1: zero-initial-guess sweeps skip the loads of not-yet-updated colors
+ *   "gs_minb"    blocks per SM the color-pass kernel is compiled for (2 or 3)
+ *   "wave"       bit mask (1 fp64, 2 fp32): forward sweeps as one dataflow kernel
+ *                (bitwise identical; default 1) */
 int hpg_set_option(hpg_ctx* ctx, const char* key, int64_t value);
 
 /* NVLink peer memory (csrc/hpg_p2p.cuh).  Collective setup, nranks > 1:

@@ -17,6 +17,7 @@
 #include "hpg_coarse.cuh"
 #include "hpg_cgs.cuh"
 #include "hpg_p2p.cuh"
+#include "hpg_wave.cuh"
 
 using hpg::Geom;
 
@@ -153,6 +154,10 @@ struct Level {
   int32_t* f2c = nullptr;  // (coarse levels, general colorings) fine row of coarse row i
   int32_t* perm_d = nullptr;   // general coloring tables (null: greedy closed form)
   int32_t* iperm_d = nullptr;
+  hpg::WaveLevel wave;         // dataflow sweep plan (valid when wave_ok)
+  bool wave_ok = false;
+  int32_t* wave_items = nullptr;
+  unsigned int* wave_done = nullptr;
   uint8_t* hflag = nullptr;    // rows reading halo slots (multi-rank)
   int32_t* bnd = nullptr;      // all such rows
   int64_t nbnd = 0;
@@ -220,6 +225,13 @@ struct hpg_ctx {
   bool general = false;  // some level uses an explicit (non-greedy) coloring
   bool graphs = true;    // replay captured V-cycles (single rank)
   bool known_zero = true;  // zero sweeps skip loads of known zeros (same arithmetic)
+  // sweeps as one dataflow kernel (hpg_wave.cuh) where the layout allows; bit 0:
+  // fp64 sweeps, bit 1: fp32.  Measured at 256^3: fp64 sweep -9%, fp32 +19%
+  int wave = 1;
+  int64_t wave_min_rows = 0;
+  int wave_lag = 8;
+  bool wave_coh = false;
+  int wave_blocks[2] = {0, 0};
   std::vector<GraphEntry> gcache;
   uint64_t gclock = 0;
   bool pdl = true;
@@ -417,6 +429,25 @@ int gs_pass_launch(hpg_ctx* c, Level& L, int64_t a, int64_t cnt, const T* r, T* 
   return HPG_OK;
 }
 
+template <typename T>
+const void* wave_fn(bool coh) {
+  return coh ? (const void*)hpg::k_gs_wave<T, true> : (const void*)hpg::k_gs_wave<T, false>;
+}
+
+template <typename T>
+int gs_wave_launch(hpg_ctx* c, Level& L, const T* r, T* z, int zero) {
+  const int blocks = c->wave_blocks[sizeof(T) == 4];
+  const int32_t* cols = L.cols;
+  const T* vals = vals_of<T>(L);
+  int64_t ld = L.ld;
+  void* args[] = {(void*)&cols, (void*)&vals, (void*)&ld, (void*)&r, (void*)&z, (void*)&L.wave, (void*)&zero};
+  const void* fn = wave_fn<T>(c->wave_coh);
+  CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(hpg::kWaveRows), args, 0,
+                                       c->stream));
+  ++c->launches;
+  return HPG_OK;
+}
+
 // One forward multicolor sweep (ref: smoother.py:78-114).  Multi-rank: the
 // exchange of z overlaps color 0's interior rows, then color 0's boundary rows,
 // then colors 1.. (block-Jacobi across ranks: one exchange per sweep).
@@ -427,6 +458,23 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
   Level& L = c->lev[l];
   const int prec = sizeof(T) == 8 ? HPG_F64 : HPG_F32;
   int first = 0, rc;
+  const bool use_wave = (c->wave >> (sizeof(T) == 4)) & 1 && L.wave_ok && L.n >= c->wave_min_rows && c->wave_blocks[sizeof(T) == 4] > 0 &&
+                        !(overlapped(c, l) && !zero);
+  if (use_wave) {
+    if (zero) {
+      if (L.n_ext > L.n) {  // zero initial guess: clear the halo tail; rows are all written
+        CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n_ext - L.n, 4)), 256, z + L.n, L.n_ext - L.n));
+        ++c->launches;
+      }
+      if (!c->known_zero) {
+        CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n, 4)), 256, z, L.n));
+        ++c->launches;
+      }
+    } else if ((rc = do_exchange(c, l, prec, z))) {
+      return rc;
+    }
+    return gs_wave_launch<T>(c, L, r, z, zero && c->known_zero);
+  }
   if (zero && c->known_zero) {
     // zero initial guess (ref: smoother.py:95-96): only the halo tail is cleared;
     // every owned row is written by its color pass, which forms v * 0 for the
@@ -772,7 +820,8 @@ int gemv_t(hpg_ctx* c, const T* Q, int64_t ldq, int k, const double* y, T* out) 
 void free_level(Level& L) {
   for (void* p : {(void*)L.cols, (void*)L.v64, (void*)L.v32, (void*)L.inj, (void*)L.send_idx, L.send_buf,
                   (void*)L.z64, (void*)L.z32, (void*)L.r64, (void*)L.r32, (void*)L.hflag, (void*)L.bnd,
-                  (void*)L.bnd0, (void*)L.f2c, (void*)L.perm_d, (void*)L.iperm_d})
+                  (void*)L.bnd0, (void*)L.f2c, (void*)L.perm_d, (void*)L.iperm_d, (void*)L.wave_items,
+                  (void*)L.wave_done})
     if (p) cudaFree(p);
   L = Level();
 }
@@ -848,6 +897,50 @@ int build_structure(hpg_ctx* c, Level& L, bool first) {
   return HPG_OK;
 }
 
+// Dataflow sweep plan for a greedy (closed-form) level with every extent >= 2:
+// color c = px + 2 py + 4 pz; its half-plane Z holds hx(px) * hy(py) rows.
+int build_wave(hpg_ctx* c, Level& L) {
+  L.wave_ok = false;
+  const Geom& g = L.g;
+  if (g.perm_tab || g.ncolors != 8 || g.lx < 2 || g.ly < 2 || g.lz < 2 || !L.n) return HPG_OK;
+  hpg::WaveLevel& w = L.wave;
+  memset(&w, 0, sizeof w);
+  w.ncolors = 8;
+  for (int k = 0; k <= hpg::kMaxColors; ++k) w.off[k] = g.off[k];
+  int maxp = 0;
+  for (int col = 0; col < 8; ++col) {
+    const int px = col & 1, py = (col >> 1) & 1, pz = (col >> 2) & 1;
+    w.planes[col] = (g.lz - pz + 1) / 2;
+    w.plane[col] = (int64_t)((g.lx - px + 1) / 2) * ((g.ly - py + 1) / 2);
+    w.chunks[col] = (int)cdiv(w.plane[col], hpg::kWaveRows);
+    if (w.chunks[col] > 255 || w.planes[col] > 65535) return HPG_OK;
+    maxp = std::max(maxp, w.planes[col]);
+  }
+  w.maxplanes = maxp;
+  // wavefront order t = Z + lag * c: a larger lag puts an item's producers
+  // (color c-1, planes Z-1..Z+1) further ahead in the deal, so co-resident
+  // blocks rarely wait; the live window of z grows as lag * 8 half-planes
+  const int lag = c->wave_lag;
+  std::vector<int32_t> items;
+  for (int t = 0; t < maxp + lag * 8; ++t)
+    for (int col = 0; col < 8; ++col) {
+      const int Z = t - lag * col;
+      if (Z < 0 || Z >= w.planes[col]) continue;
+      for (int q = 0; q < w.chunks[col]; ++q) items.push_back((col << 24) | (Z << 8) | q);
+    }
+  w.nitems = (int64_t)items.size();
+  int rc;
+  if ((rc = dmalloc(&L.wave_items, items.size() * 4, &L.bytes))) return rc;
+  if ((rc = dmalloc(&L.wave_done, ((size_t)8 * maxp + 2) * 4, &L.bytes))) return rc;
+  CUDA_TRY(cudaMemcpy(L.wave_items, items.data(), items.size() * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemset(L.wave_done, 0, ((size_t)8 * maxp + 2) * 4));
+  w.items = L.wave_items;
+  w.done = L.wave_done;
+  w.ctl = L.wave_done + (size_t)8 * maxp;
+  L.wave_ok = true;
+  return HPG_OK;
+}
+
 int build_level(hpg_ctx* c, Level& L, const int dims[3]) {
   L.g = make_geom(dims, c->coords, c->procs);
   L.n = L.g.n;
@@ -864,6 +957,7 @@ int build_level(hpg_ctx* c, Level& L, const int dims[3]) {
   CUDA_TRY(cudaMemsetAsync(L.v64, 0, slots * 8, c->stream));
   CUDA_TRY(cudaMemsetAsync(L.v32, 0, slots * 4, c->stream));
   if ((rc = build_structure(c, L, true))) return rc;
+  if ((rc = build_wave(c, L))) return rc;
   if ((rc = dmalloc(&L.z64, L.n_ext * 8, &L.bytes))) return rc;
   if ((rc = dmalloc(&L.z32, L.n_ext * 4, &L.bytes))) return rc;
   if ((rc = dmalloc(&L.r64, L.n * 8, &L.bytes))) return rc;
@@ -1068,6 +1162,21 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
   {
     const char* e = getenv("HPG_TAIL_ROWS");
     c->tail_rows = e ? atoll(e) : (int64_t)0;  // measured: per-pass PDL kernels win at 256^3
+    const char* wv = getenv("HPG_WAVE");
+    if (wv) c->wave = atoi(wv);
+    const char* wl = getenv("HPG_WAVE_LAG");
+    if (wl) c->wave_lag = std::max(1, atoi(wl));
+    const char* wc = getenv("HPG_WAVE_COH");
+    if (wc) c->wave_coh = wc[0] != '0';
+    const char* wm = getenv("HPG_WAVE_MIN_ROWS");
+    if (wm) c->wave_min_rows = atoll(wm);
+    int pw = 0;
+    auto occ = [&](const void* fn) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pw, fn, hpg::kWaveRows, 0);
+      return pw * sms;
+    };
+    c->wave_blocks[0] = std::min(occ(wave_fn<double>(true)), occ(wave_fn<double>(false)));
+    c->wave_blocks[1] = std::min(occ(wave_fn<float>(true)), occ(wave_fn<float>(false)));
     const char* f = getenv("HPG_CGS_FUSED");
     c->cgs_fused = !(f && f[0] == '0');
     const char* mb = getenv("HPG_GS_MINB");
@@ -1225,6 +1334,7 @@ int hpg_set_coloring(hpg_ctx* c, int l, int ncolors, const int64_t* offsets, con
   L.g.ncolors = ncolors;
   for (int k = 0; k <= hpg::kMaxColors; ++k) L.g.off[k] = k <= ncolors ? offsets[k] : L.n;
   c->general = true;
+  L.wave_ok = false;  // the dataflow plan needs the closed-form (greedy) layout
   if ((rc = build_structure(c, L, false))) return rc;
   // injection maps of the coarse levels that touch this one
   for (int cl = std::max(1, l); cl <= std::min(l + 1, c->nlev - 1); ++cl) {
@@ -1512,6 +1622,8 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   else if (!strcmp(key, "p2p")) c->p2p = value != 0 && !c->peer_sym.empty();
   else if (!strcmp(key, "overlap_rows")) c->overlap_rows = value;
   else if (!strcmp(key, "gs_minb")) c->gs_minb = (int)value;
+  else if (!strcmp(key, "wave")) c->wave = (int)value;
+  else if (!strcmp(key, "wave_min_rows")) c->wave_min_rows = value;
   else if (!strcmp(key, "known_zero")) c->known_zero = value != 0;
   else if (!strcmp(key, "graphs")) {
     c->graphs = value != 0;
