@@ -82,7 +82,9 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
 int hpg_destroy(hpg_ctx* ctx);
 void* hpg_stream(hpg_ctx* ctx);   /* cudaStream_t of the compute stream */
 
-/* info: n, n_ext, nnz, ncolors, offsets[9], halo_size, ld, nneighbours, device_bytes */
+/* info: n, n_ext, nnz, ncolors, offsets[9], halo_size, ld, nneighbours, device_bytes,
+ *       zero_sweep_slots (slots a zero-initial-guess sweep streams, sum over colors
+ *       of lower width x rows; 27 n when the lower split is absent) */
 int hpg_level_info(hpg_ctx* ctx, int level, int64_t* info, int ninfo);
 /* Copy a device level back in the reference layout (host buffers [n][27]). */
 int hpg_export_level(hpg_ctx* ctx, int level, double* values, int32_t* col_idx,
@@ -146,8 +148,8 @@ int hpg_allreduce_host(hpg_ctx* ctx, double* vals, int n);
 int64_t hpg_launch_count(hpg_ctx* ctx);
 /* Per-motif CUDA-event timers (ref: metrics.py:111-143 Tally).  mode 1 enable,
  * 0 disable, 2 synchronise + ADD seconds per motif into seconds[8]
- * (GS, SpMV, Ortho, Restriction, Prolongation, Vector ops, GS level-0 subset,
- * reserved) and reset.                                                      */
+ * (GS, SpMV, Ortho, Restriction, Prolongation, Vector ops, and two subsets of
+ * GS: level-0 full sweeps, level-0 zero-initial-guess sweeps) and reset.     */
 int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
 /* Tuning switches (results are identical up to reduction order):
  *   "cgs_fused"  1: single-rank CGS2 as one cooperative bulk-copy kernel, 0: per-pass kernels

@@ -18,6 +18,7 @@
 #include "hpg_cgs.cuh"
 #include "hpg_p2p.cuh"
 #include "hpg_wave.cuh"
+#include "hpg_lower.cuh"
 
 using hpg::Geom;
 
@@ -158,6 +159,14 @@ struct Level {
   bool wave_ok = false;
   int32_t* wave_items = nullptr;
   unsigned int* wave_done = nullptr;
+  // strictly-lower part per color for zero-initial-guess sweeps (hpg_lower.cuh)
+  bool lower_ok = false;
+  hpg::LowerColor lc[hpg::kMaxColors];
+  int32_t* lcols = nullptr;
+  double* lv64 = nullptr;
+  float* lv32 = nullptr;
+  double* dg64 = nullptr;
+  float* dg32 = nullptr;
   uint8_t* hflag = nullptr;    // rows reading halo slots (multi-rank)
   int32_t* bnd = nullptr;      // all such rows
   int64_t nbnd = 0;
@@ -224,6 +233,7 @@ struct hpg_ctx {
   bool cgs_fused = true;
   bool general = false;  // some level uses an explicit (non-greedy) coloring
   bool graphs = true;    // replay captured V-cycles (single rank)
+  bool lower = true;       // zero sweeps stream only the strictly-lower part (hpg_lower.cuh)
   bool known_zero = true;  // zero sweeps skip loads of known zeros (same arithmetic)
   // sweeps as one dataflow kernel (hpg_wave.cuh) where the layout allows; bit 0:
   // fp64 sweeps, bit 1: fp32.  Measured at 256^3: fp64 sweep -9%, fp32 +19%
@@ -247,7 +257,7 @@ struct hpg_ctx {
 
 namespace {
 
-enum Motif { M_GS = 0, M_SPMV = 1, M_ORTHO = 2, M_RESTRICT = 3, M_PROLONG = 4, M_VEC = 5, M_GS_L0 = 6 };
+enum Motif { M_GS = 0, M_SPMV = 1, M_ORTHO = 2, M_RESTRICT = 3, M_PROLONG = 4, M_VEC = 5, M_GS_L0 = 6, M_GS_L0Z = 7 };
 
 // RAII motif region: records an event pair on the compute stream when timing is on
 struct Timed {
@@ -430,6 +440,29 @@ int gs_pass_launch(hpg_ctx* c, Level& L, int64_t a, int64_t cnt, const T* r, T* 
 }
 
 template <typename T>
+int gs_lower_launch(hpg_ctx* c, Level& L, int col, const T* r, T* z) {
+  const hpg::LowerColor& lc = L.lc[col];
+  const int64_t a = L.g.off[col], cnt = L.g.off[col + 1] - a;
+  if (cnt <= 0) return HPG_OK;
+  const int32_t* lcols = L.lcols + lc.base;
+  const T* lv = (sizeof(T) == 8 ? (const T*)L.lv64 : (const T*)L.lv32) + lc.base;
+  const T* dg = sizeof(T) == 8 ? (const T*)L.dg64 : (const T*)L.dg32;
+  const int g = grid_for(cnt);
+  cudaError_t e;
+  if (lc.w <= 2) e = launch_pdl(c, hpg::k_gs_lower<T, 2>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
+  else if (lc.w <= 4) e = launch_pdl(c, hpg::k_gs_lower<T, 4>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
+  else if (lc.w <= 8) e = launch_pdl(c, hpg::k_gs_lower<T, 8>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
+  else if (lc.w <= 12) e = launch_pdl(c, hpg::k_gs_lower<T, 12>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
+  else if (lc.w <= 16) e = launch_pdl(c, hpg::k_gs_lower<T, 16>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
+  else if (lc.w <= 20) e = launch_pdl(c, hpg::k_gs_lower<T, 20>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
+  else if (lc.w <= 24) e = launch_pdl(c, hpg::k_gs_lower<T, 24>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
+  else e = launch_pdl(c, hpg::k_gs_lower<T, 27>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
+  CUDA_TRY(e);
+  ++c->launches;
+  return HPG_OK;
+}
+
+template <typename T>
 const void* wave_fn(bool coh) {
   return coh ? (const void*)hpg::k_gs_wave<T, true> : (const void*)hpg::k_gs_wave<T, false>;
 }
@@ -454,10 +487,23 @@ int gs_wave_launch(hpg_ctx* c, Level& L, const T* r, T* z, int zero) {
 template <typename T>
 int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
   Timed tm(c, M_GS);
-  Timed tm0(c, l == 0 ? M_GS_L0 : -1);  // level-0 sweeps also timed alone (bench roofline)
   Level& L = c->lev[l];
+  // level-0 sweeps also timed alone (bench roofline): full sweeps and zero-guess
+  // (strictly-lower) sweeps apart, they run different kernels
+  Timed tm0(c, l != 0 ? -1 : (zero && c->lower && L.lower_ok) ? M_GS_L0Z : M_GS_L0);
   const int prec = sizeof(T) == 8 ? HPG_F64 : HPG_F32;
   int first = 0, rc;
+  if (zero && c->lower && L.lower_ok) {
+    // zero initial guess: only the strictly-lower part of each color contributes
+    // (hpg_lower.cuh, bitwise equal); the halo tail is still cleared for later users
+    if (L.n_ext > L.n) {
+      CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n_ext - L.n, 4)), 256, z + L.n, L.n_ext - L.n));
+      ++c->launches;
+    }
+    for (int col = 0; col < L.g.ncolors; ++col)
+      if ((rc = gs_lower_launch<T>(c, L, col, r, z))) return rc;
+    return HPG_OK;
+  }
   const bool use_wave = (c->wave >> (sizeof(T) == 4)) & 1 && L.wave_ok && L.n >= c->wave_min_rows && c->wave_blocks[sizeof(T) == 4] > 0 &&
                         !(overlapped(c, l) && !zero);
   if (use_wave) {
@@ -821,7 +867,7 @@ void free_level(Level& L) {
   for (void* p : {(void*)L.cols, (void*)L.v64, (void*)L.v32, (void*)L.inj, (void*)L.send_idx, L.send_buf,
                   (void*)L.z64, (void*)L.z32, (void*)L.r64, (void*)L.r32, (void*)L.hflag, (void*)L.bnd,
                   (void*)L.bnd0, (void*)L.f2c, (void*)L.perm_d, (void*)L.iperm_d, (void*)L.wave_items,
-                  (void*)L.wave_done})
+                  (void*)L.wave_done, (void*)L.lcols, (void*)L.lv64, (void*)L.lv32, (void*)L.dg64, (void*)L.dg32})
     if (p) cudaFree(p);
   L = Level();
 }
@@ -835,6 +881,49 @@ int dmalloc(P** p, size_t bytes, size_t* acc) {
   return HPG_OK;
 }
 
+// Strictly-lower part of every color block (hpg_lower.cuh), from the ELL rows.
+int build_lower(hpg_ctx* c, Level& L) {
+  L.lower_ok = false;
+  for (void* p : {(void*)L.lcols, (void*)L.lv64, (void*)L.lv32, (void*)L.dg64, (void*)L.dg32})
+    if (p) cudaFree(p);
+  L.lcols = nullptr, L.lv64 = nullptr, L.lv32 = nullptr, L.dg64 = nullptr, L.dg32 = nullptr;
+  const int nc = L.g.ncolors;
+  char* scratch = nullptr;  // setup-time scratch: widths, then the per-color table
+  CUDA_TRY(cudaMalloc(&scratch, 4096));
+  int* wd = (int*)scratch;
+  CUDA_TRY(cudaMemsetAsync(wd, 0, hpg::kMaxColors * sizeof(int), c->stream));
+  hpg::k_lower_count<<<grid_for(L.n), 256, 0, c->stream>>>(L.g, L.ld, L.cols, L.v64, wd);
+  LAUNCH_CHECK();
+  int w[hpg::kMaxColors] = {0};
+  CUDA_TRY(cudaMemcpyAsync(w, wd, sizeof w, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  int64_t tot = 0;
+  for (int k = 0; k < nc; ++k) {
+    if (w[k] > 27) return fail(HPG_E_ARG, "lower width %d", w[k]);
+    L.lc[k].w = w[k];
+    L.lc[k].ldc = pad_ld(L.g.off[k + 1] - L.g.off[k]);  // odd multiple of 128 B: no L2-slice aliasing
+    L.lc[k].base = tot;
+    tot += (int64_t)w[k] * L.lc[k].ldc;
+  }
+  int rc;
+  size_t* acc = nullptr;  // accounted in L.bytes below
+  if ((rc = dmalloc(&L.lcols, std::max<int64_t>(1, tot) * 4, acc))) return rc;
+  if ((rc = dmalloc(&L.lv64, std::max<int64_t>(1, tot) * 8, acc))) return rc;
+  if ((rc = dmalloc(&L.lv32, std::max<int64_t>(1, tot) * 4, acc))) return rc;
+  if ((rc = dmalloc(&L.dg64, L.n * 8, acc))) return rc;
+  if ((rc = dmalloc(&L.dg32, L.n * 4, acc))) return rc;
+  L.bytes += tot * 16 + L.n * 12;
+  hpg::LowerColor* lcd = (hpg::LowerColor*)(scratch + 1024);
+  CUDA_TRY(cudaMemcpyAsync(lcd, L.lc, nc * sizeof(hpg::LowerColor), cudaMemcpyHostToDevice, c->stream));
+  hpg::k_lower_fill<<<grid_for(L.n), 256, 0, c->stream>>>(L.g, L.ld, L.cols, L.v64, lcd, L.lcols, L.lv64, L.lv32,
+                                                           L.dg64, L.dg32);
+  LAUNCH_CHECK();
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  cudaFree(scratch);
+  L.lower_ok = true;
+  return HPG_OK;
+}
+
 // (Re)build a level's permutation-dependent structure: ELL rows, send lists and
 // the interior/boundary split.  `first` allocates the send/split buffers.
 int build_structure(hpg_ctx* c, Level& L, bool first) {
@@ -842,6 +931,7 @@ int build_structure(hpg_ctx* c, Level& L, bool first) {
   if (L.n) {
     hpg::k_build_level<<<grid_for(L.n, 128), 128, 0, c->stream>>>(L.g, L.ld, L.cols, L.v64, L.v32);
     LAUNCH_CHECK();
+    if ((rc = build_lower(c, L))) return rc;
   }
   // halo plan: one send list per neighbour, in ascending neighbour rank
   struct Tmp {
@@ -1181,6 +1271,8 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     c->cgs_fused = !(f && f[0] == '0');
     const char* mb = getenv("HPG_GS_MINB");
     if (mb) c->gs_minb = atoi(mb);
+    const char* lw = getenv("HPG_LOWER");
+    if (lw) c->lower = lw[0] != '0';
     const char* kz = getenv("HPG_KNOWN_ZERO");
     if (kz) c->known_zero = kz[0] != '0';
     const char* gr = getenv("HPG_GRAPHS");
@@ -1257,7 +1349,12 @@ int hpg_level_info(hpg_ctx* c, int l, int64_t* info, int ninfo) {
   tmp[14] = L.ld;
   tmp[15] = (int64_t)L.nbrs.size();
   tmp[16] = (int64_t)L.bytes;
-  for (int k = 0; k < ninfo && k < 17; ++k) info[k] = tmp[k];
+  // slots a zero-initial-guess sweep streams: sum_c W_c * rows_c (27 n without the lower split)
+  int64_t ls = 0;
+  for (int k = 0; k < L.g.ncolors; ++k)
+    ls += (L.lower_ok ? L.lc[k].w : hpg::kWidth) * (L.g.off[k + 1] - L.g.off[k]);
+  tmp[17] = ls;
+  for (int k = 0; k < ninfo && k < 18; ++k) info[k] = tmp[k];
   return HPG_OK;
 }
 
@@ -1625,6 +1722,7 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   else if (!strcmp(key, "wave")) c->wave = (int)value;
   else if (!strcmp(key, "wave_min_rows")) c->wave_min_rows = value;
   else if (!strcmp(key, "known_zero")) c->known_zero = value != 0;
+  else if (!strcmp(key, "lower")) c->lower = value != 0;
   else if (!strcmp(key, "graphs")) {
     c->graphs = value != 0;
     for (auto& e : c->gcache) cudaGraphExecDestroy(e.exec);

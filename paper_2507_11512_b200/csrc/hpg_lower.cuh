@@ -1,0 +1,121 @@
+// Zero-initial-guess Gauss-Seidel sweep on the strictly-lower part.
+//
+// With z = 0 on entry (ref: smoother.py:95-96), a row of color c sees new values
+// only at columns of colors < c; every other product of its 27-slot sum is
+// v * 0 = +-0 (the diagonal's is 0 * z_i by the reference's zeroed offvals,
+// padding is 0 * z[0]).  The accumulator starts at +0 and can never become -0
+// (only -0 + -0 is -0), so adding a +-0 product never changes it: the slot-order
+// sum of the lower entries alone is the full row sum BIT FOR BIT.  The sweep
+// therefore streams only the lower entries (about half of the matrix, ~13 of 27
+// slots per row on the 8-color lattice) plus a diagonal vector, instead of every
+// slot.  The flop model is unchanged (ref: metrics.py counts the full sweep).
+//
+// Layout per level and color block c: slot-major ELL [W_c][ldc_c] of the row's
+// lower entries in their original slot order, padded with (column 0, value 0);
+// W_c = max lower count over the block.  dg = a_ii per row.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hpg_geom.h"
+#include "hpg_kernels.cuh"
+
+namespace hpg {
+
+struct LowerColor {
+  int64_t base;  // first element of this color's [W][ldc] block
+  int64_t ldc;   // row stride (rows of the color padded to 32)
+  int w;         // width
+};
+
+__device__ __forceinline__ int color_of_row(const Geom& g, int64_t i) {
+  int c = 0;
+  while (c + 1 < g.ncolors && i >= g.off[c + 1]) ++c;
+  return c;
+}
+
+__device__ __forceinline__ bool is_lower(int32_t col, double v, int64_t lim) {
+  return col >= 0 && col < lim && v != 0.0;  // off-diagonal (diag is ~col), stored, earlier color
+}
+
+// W_c = max over the color block of the lower-entry count
+__global__ void k_lower_count(Geom g, int64_t ld, const int32_t* __restrict__ cols, const double* __restrict__ v64,
+                              int* __restrict__ width) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  const int c = color_of_row(g, i);
+  int k = 0;
+  for (int s = 0; s < kWidth; ++s) k += is_lower(cols[s * ld + i], v64[s * ld + i], g.off[c]);
+  atomicMax(width + c, k);
+}
+
+__global__ void k_lower_fill(Geom g, int64_t ld, const int32_t* __restrict__ cols, const double* __restrict__ v64,
+                             const LowerColor* __restrict__ lc, int32_t* __restrict__ lcols,
+                             double* __restrict__ lv64, float* __restrict__ lv32, double* __restrict__ dg64,
+                             float* __restrict__ dg32) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  const int c = color_of_row(g, i);
+  const LowerColor L = lc[c];
+  const int64_t j = i - g.off[c];
+  int k = 0;
+  for (int s = 0; s < kWidth; ++s) {
+    const int32_t col = cols[s * ld + i];
+    const double v = v64[s * ld + i];
+    if (col < 0) {
+      dg64[i] = v;
+      dg32[i] = (float)v;
+    }
+    if (is_lower(col, v, g.off[c])) {
+      lcols[L.base + k * L.ldc + j] = col;
+      lv64[L.base + k * L.ldc + j] = v;
+      lv32[L.base + k * L.ldc + j] = (float)v;
+      ++k;
+    }
+  }
+  for (; k < L.w; ++k) {
+    lcols[L.base + k * L.ldc + j] = 0;
+    lv64[L.base + k * L.ldc + j] = 0.0;
+    lv32[L.base + k * L.ldc + j] = 0.0f;
+  }
+}
+
+// One color of the zero-initial-guess sweep: z_i = (r_i - sum_lower v z) / a_ii.
+// WMAX >= w; the loads are predicated on the (uniform) width.
+#ifndef HPG_LOWER_MINB
+#define HPG_LOWER_MINB 2
+#endif
+template <typename T, int WMAX>
+__global__ void __launch_bounds__(256, sizeof(T) == 8 ? 2 : HPG_LOWER_MINB) k_gs_lower(const int32_t* __restrict__ lcols, const T* __restrict__ lvals,
+                                                     int64_t ldc, int w, int64_t row0, int64_t nrows,
+                                                     const T* __restrict__ dg, const T* __restrict__ r, T* z) {
+  pdl_trigger();
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nrows) return;
+  const int64_t i = row0 + j;
+  const uint64_t pol = stream_policy();
+  int32_t c[WMAX > 0 ? WMAX : 1];
+  T v[WMAX > 0 ? WMAX : 1];
+#pragma unroll
+  for (int s = 0; s < WMAX; ++s)
+    if (s < w) c[s] = ld_stream(lcols + s * ldc + j, pol);
+#pragma unroll
+  for (int s = 0; s < WMAX; ++s)
+    if (s < w) v[s] = ld_stream(lvals + s * ldc + j, pol);
+  const T d = dg[i];
+  // z of the earlier colors (and r) are written by previous kernels
+  if (w > 0) pdl_wait_after(v[0]);
+  else pdl_wait();
+  const T ri = r[i];
+  T g[WMAX > 0 ? WMAX : 1];
+#pragma unroll
+  for (int s = 0; s < WMAX; ++s)
+    if (s < w) g[s] = z[c[s]];
+  T acc = T(0);
+#pragma unroll
+  for (int s = 0; s < WMAX; ++s)
+    if (s < w) acc = add_rn(acc, mul_rn(v[s], g[s]));
+  z[i] = div_rn(sub_rn(ri, acc), d);
+}
+
+}  // namespace hpg

@@ -10,7 +10,7 @@ from . import _lib
 from .comm import runtime
 
 INFO_KEYS = ("n", "n_ext", "nnz", "ncolors") + tuple(f"off{i}" for i in range(9)) + \
-    ("halo", "ld", "nneighbours", "device_bytes")
+    ("halo", "ld", "nneighbours", "device_bytes", "zero_sweep_slots")
 
 
 class Context:
@@ -59,8 +59,8 @@ class Context:
         _lib.check(getattr(_lib.lib(), name)(self.h, *args))
 
     def _level_info(self, l):
-        buf = np.zeros(17, dtype=np.int64)
-        self.call("hpg_level_info", l, buf.ctypes.data_as(C.POINTER(C.c_int64)), 17)
+        buf = np.zeros(len(INFO_KEYS), dtype=np.int64)
+        self.call("hpg_level_info", l, buf.ctypes.data_as(C.POINTER(C.c_int64)), len(INFO_KEYS))
         return dict(zip(INFO_KEYS, (int(v) for v in buf)))
 
     def level_info(self, l):

@@ -95,9 +95,15 @@ class Tally:
         self.flops = {m: 0 for m in MOTIFS}
         self.bytes = {m: 0 for m in MOTIFS}
         self.seconds = {m: 0.0 for m in MOTIFS}
-        self.gs_level0_seconds = 0.0   # additive: level-0 sweeps alone (subset of GS)
+        # subsets of GS timed alone for the bench roofline: level-0 full sweeps
+        # (k_gs_pass, model bytes) and level-0 zero-initial-guess sweeps
+        # (k_gs_lower, the bytes that kernel streams)
+        self.gs_level0_seconds = 0.0
         self.gs_level0_bytes = 0
         self.gs_level0_sweeps = 0
+        self.gs_level0z_seconds = 0.0
+        self.gs_level0z_bytes = 0
+        self.gs_level0z_sweeps = 0
 
     def add(self, kernel, dtype, motif=None, **sizes):
         bucket = motif or kernel_motif(kernel)
@@ -119,6 +125,7 @@ class Tally:
         for m, s in zip(MOTIFS, sec):
             self.seconds[m] += float(s)
         self.gs_level0_seconds += float(sec[6])
+        self.gs_level0z_seconds += float(sec[7])
 
     def total_flops(self):
         return sum(self.flops.values())
@@ -134,6 +141,9 @@ class Tally:
         self.gs_level0_seconds = 0.0
         self.gs_level0_bytes = 0
         self.gs_level0_sweeps = 0
+        self.gs_level0z_seconds = 0.0
+        self.gs_level0z_bytes = 0
+        self.gs_level0z_sweeps = 0
 
 
 def sum_motif_dicts(dicts):

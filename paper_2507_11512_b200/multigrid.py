@@ -92,17 +92,29 @@ def count_vcycle(h, tally, dtype):
         A = h.levels[lev].A_hi
         last = lev == nl - 1
         sweeps = sw.nu_c if last else sw.nu1 + sw.nu2
-        for _ in range(sweeps):
+        for k in range(sweeps):
             tally.add("gs_sweep", dtype, nnz=A.nnz_total, n=A.n_rows)
             if lev == 0 and hasattr(tally, "gs_level0_bytes"):
-                from .metrics import count_bytes
-                tally.gs_level0_bytes += count_bytes("gs_sweep", np.dtype(dtype).itemsize,
-                                                     nnz=A.nnz_total, n=A.n_rows)
-                tally.gs_level0_sweeps += 1
+                w = np.dtype(dtype).itemsize
+                if k == 0 and (last or sw.nu1 > 0) and h.ctx is not None:
+                    # the first sweep starts from z = 0: the strictly-lower kernel streams
+                    # its slots (index + value) and r, a_ii, z once each
+                    tally.gs_level0z_bytes += zero_sweep_bytes(h, w)
+                    tally.gs_level0z_sweeps += 1
+                else:
+                    from .metrics import count_bytes
+                    tally.gs_level0_bytes += count_bytes("gs_sweep", w, nnz=A.nnz_total, n=A.n_rows)
+                    tally.gs_level0_sweeps += 1
         if not last:
             nxt = h.levels[lev + 1]
             tally.add("restrict_fused", dtype, nnz=nxt.inject_nnz, n_c=nxt.A_hi.n_rows)
             tally.add("prolong_add", dtype, n_c=nxt.A_hi.n_rows)
+
+
+def zero_sweep_bytes(h, w):
+    """Bytes one level-0 zero-initial-guess sweep streams (csrc/hpg_lower.cuh)."""
+    info = h.ctx.level_info(0)
+    return info["zero_sweep_slots"] * (4 + w) + 4 * info["n"] * w
 
 
 def _inject_nnz(domain):

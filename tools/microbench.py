@@ -15,6 +15,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--local", type=int, default=256)
     p.add_argument("--reps", type=int, default=20)
+    p.add_argument("--brief", default="", help="label: print only the headline keys on one line")
     a = p.parse_args()
     import torch
     from paper_2507_11512_b200 import _lib
@@ -26,7 +27,8 @@ def main():
     st = ctx.stream
     n, ne = lv.A_hi.n_rows, lv.A_hi.n_cols_extended
     nnz = lv.A_hi.nnz_total
-    out = {"local": a.local, "tail_rows": os.environ.get("HPG_TAIL_ROWS", "default")}
+    out = {"local": a.local, "tail_rows": os.environ.get("HPG_TAIL_ROWS", "default"),
+           "zero_sweep_slots_per_row": ctx.level_info(0)["zero_sweep_slots"] / n}
 
     def timeit(fn, reps=a.reps):
         fn()
@@ -56,6 +58,7 @@ def main():
     us = timeit(lambda: ctx.call("hpg_gs_sweep", 0, _lib.F32, _lib.ptr(r32), _lib.ptr(z32), 0))
     out["gs_sweep_L0_f32_us"] = us
     out["gs_sweep_L0_f32_GBs"] = (nnz * 8 + 3 * n * 4) / us / 1e3
+    out["gs_sweep0_L0_f32_us"] = timeit(lambda: ctx.call("hpg_gs_sweep", 0, _lib.F32, _lib.ptr(r32), _lib.ptr(z32), 1))
     z64 = torch.zeros(ne, device="cuda", dtype=torch.float64)
     r64b = torch.randn(n, device="cuda", dtype=torch.float64)
     us = timeit(lambda: ctx.call("hpg_gs_sweep", 0, _lib.F64, _lib.ptr(r64b), _lib.ptr(z64), 0))
@@ -65,6 +68,26 @@ def main():
     us = timeit(lambda: ctx.call("hpg_spmv", 0, _lib.F64, _lib.ptr(x64), _lib.ptr(y64)))
     out["spmv_f64_us"] = us
     out["spmv_f64_GBs"] = (nnz * 12 + 2 * n * 8) / us / 1e3
+    # every level's sweeps, restriction and prolongation (fp32), warm
+    for li in range(1, len(hier.levels)):
+        A = hier.levels[li].A_lo
+        nl, nel = A.n_rows, A.n_cols_extended
+        rl = torch.randn(nl, device="cuda", dtype=torch.float32)
+        zl = torch.zeros(nel, device="cuda", dtype=torch.float32)
+        out[f"gs_sweep_L{li}_f32_us"] = timeit(
+            lambda: ctx.call("hpg_gs_sweep", li, _lib.F32, _lib.ptr(rl), _lib.ptr(zl), 0))
+        out[f"gs_sweep0_L{li}_f32_us"] = timeit(
+            lambda: ctx.call("hpg_gs_sweep", li, _lib.F32, _lib.ptr(rl), _lib.ptr(zl), 1))
+    for li in range(len(hier.levels) - 1):
+        Af, Ac = hier.levels[li].A_lo, hier.levels[li + 1].A_lo
+        rf = torch.randn(Af.n_rows, device="cuda", dtype=torch.float32)
+        zf = torch.randn(Af.n_cols_extended, device="cuda", dtype=torch.float32)
+        rc = torch.empty(Ac.n_rows, device="cuda", dtype=torch.float32)
+        zc = torch.randn(Ac.n_cols_extended, device="cuda", dtype=torch.float32)
+        out[f"restrict_L{li}_f32_us"] = timeit(
+            lambda: ctx.call("hpg_restrict", li, _lib.F32, _lib.ptr(rf), _lib.ptr(zf), _lib.ptr(rc)))
+        out[f"prolong_L{li}_f32_us"] = timeit(
+            lambda: ctx.call("hpg_prolong", li, _lib.F32, _lib.ptr(zf), _lib.ptr(zc)))
     us = timeit(lambda: hier.apply(r32, out=z32))
     out["vcycle_f32_us"] = us
     us = timeit(lambda: hier.apply(r64 if False else b64, out=x64))
@@ -99,7 +122,12 @@ def main():
     out["solve30_model_GBs"] = tal.total_bytes() / ms / 1e6
     out["solve30_GFs"] = tal.total_flops() / ms / 1e6
     out["solve30_motif_s"] = tal.seconds
-    print(json.dumps(out))
+    if a.brief:
+        keys = ("gs_sweep_L0_f32_us", "gs_sweep0_L0_f32_us", "zero_sweep_slots_per_row", "gs_sweep_L0_f64_us", "vcycle_f32_us", "vcycle_f64_us", "spmv_f32_us",
+                "cgs2_k30_us", "solve30_ms")
+        print(a.brief, {k: round(v, 1) for k, v in out.items() if k in keys})
+    else:
+        print(json.dumps(out))
     hier.close()
 
 
