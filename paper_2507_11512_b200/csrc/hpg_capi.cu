@@ -447,16 +447,7 @@ int gs_lower_launch(hpg_ctx* c, Level& L, int col, const T* r, T* z) {
   const int32_t* lcols = L.lcols + lc.base;
   const T* lv = (sizeof(T) == 8 ? (const T*)L.lv64 : (const T*)L.lv32) + lc.base;
   const T* dg = sizeof(T) == 8 ? (const T*)L.dg64 : (const T*)L.dg32;
-  const int g = grid_for(cnt);
-  cudaError_t e;
-  if (lc.w <= 2) e = launch_pdl(c, hpg::k_gs_lower<T, 2>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
-  else if (lc.w <= 4) e = launch_pdl(c, hpg::k_gs_lower<T, 4>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
-  else if (lc.w <= 8) e = launch_pdl(c, hpg::k_gs_lower<T, 8>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
-  else if (lc.w <= 12) e = launch_pdl(c, hpg::k_gs_lower<T, 12>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
-  else if (lc.w <= 16) e = launch_pdl(c, hpg::k_gs_lower<T, 16>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
-  else if (lc.w <= 20) e = launch_pdl(c, hpg::k_gs_lower<T, 20>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
-  else if (lc.w <= 24) e = launch_pdl(c, hpg::k_gs_lower<T, 24>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
-  else e = launch_pdl(c, hpg::k_gs_lower<T, 27>, g, 256, lcols, lv, lc.ldc, lc.w, a, cnt, dg, r, z);
+  cudaError_t e = launch_pdl(c, hpg::lower_kernel<T>(lc.w), grid_for(cnt), 256, lcols, lv, lc.ldc, a, cnt, dg, r, z);
   CUDA_TRY(e);
   ++c->launches;
   return HPG_OK;

@@ -126,7 +126,14 @@ __device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, co
   for (int s = 0; s < 27; ++s) c[s] = ld_stream(cols + s * ld + i, pol);
 #pragma unroll
   for (int s = 0; s < 27; ++s) v[s] = ld_stream(vals + s * ld + i, pol);
-  if (PDL) pdl_wait();  // x may be written by the predecessor kernel (ptxas hoists it: measured better here)
+#ifndef HPG_PIN_WAIT
+#define HPG_PIN_WAIT 0
+#endif
+  // x may be written by the predecessor kernel
+  if (PDL) {
+    if (HPG_PIN_WAIT) pdl_wait_after(v[26]);
+    else pdl_wait();  // (ptxas hoists it above the streams: measured better for the 27-slot kernels)
+  }
   T g[27];
 #pragma unroll
   for (int s = 0; s < 27; ++s) {

@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "hpg_geom.h"
 #include "hpg_kernels.cuh"
 
@@ -82,40 +84,60 @@ __global__ void k_lower_fill(Geom g, int64_t ld, const int32_t* __restrict__ col
 
 // One color of the zero-initial-guess sweep: z_i = (r_i - sum_lower v z) / a_ii.
 // WMAX >= w; the loads are predicated on the (uniform) width.
-#ifndef HPG_LOWER_MINB
-#define HPG_LOWER_MINB 2
-#endif
-template <typename T, int WMAX>
-__global__ void __launch_bounds__(256, sizeof(T) == 8 ? 2 : HPG_LOWER_MINB) k_gs_lower(const int32_t* __restrict__ lcols, const T* __restrict__ lvals,
-                                                     int64_t ldc, int w, int64_t row0, int64_t nrows,
-                                                     const T* __restrict__ dg, const T* __restrict__ r, T* z) {
+// Blocks per SM by width: narrow rows keep few loads in flight per thread, so
+// they need more resident warps to cover HBM latency (Little's law); wide rows
+// need the registers (3 W live values per thread, 5 W in fp64).
+template <typename T, int W>
+constexpr int lower_minb() {
+  return sizeof(T) == 4 ? (W <= 4 ? 8 : W <= 8 ? 6 : W <= 16 ? 4 : W <= 23 ? 3 : 2)
+                        : (W <= 4 ? 6 : W <= 8 ? 5 : W <= 12 ? 4 : W <= 16 ? 3 : 2);
+}
+
+// One color of the zero-initial-guess sweep: z_i = (r_i - sum_lower v z) / a_ii,
+// instantiated per exact width W (no predicated slots).
+template <typename T, int W>
+__global__ void __launch_bounds__(256, lower_minb<T, W>()) k_gs_lower(const int32_t* __restrict__ lcols,
+                                                                       const T* __restrict__ lvals, int64_t ldc,
+                                                                       int64_t row0, int64_t nrows,
+                                                                       const T* __restrict__ dg,
+                                                                       const T* __restrict__ r, T* z) {
   pdl_trigger();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nrows) return;
   const int64_t i = row0 + j;
   const uint64_t pol = stream_policy();
-  int32_t c[WMAX > 0 ? WMAX : 1];
-  T v[WMAX > 0 ? WMAX : 1];
+  int32_t c[W > 0 ? W : 1];
+  T v[W > 0 ? W : 1];
 #pragma unroll
-  for (int s = 0; s < WMAX; ++s)
-    if (s < w) c[s] = ld_stream(lcols + s * ldc + j, pol);
+  for (int s = 0; s < W; ++s) c[s] = ld_stream(lcols + s * ldc + j, pol);
 #pragma unroll
-  for (int s = 0; s < WMAX; ++s)
-    if (s < w) v[s] = ld_stream(lvals + s * ldc + j, pol);
+  for (int s = 0; s < W; ++s) v[s] = ld_stream(lvals + s * ldc + j, pol);
   const T d = dg[i];
   // z of the earlier colors (and r) are written by previous kernels
-  if (w > 0) pdl_wait_after(v[0]);
+  if (W > 0) pdl_wait_after(v[0]);
   else pdl_wait();
   const T ri = r[i];
-  T g[WMAX > 0 ? WMAX : 1];
+  T g[W > 0 ? W : 1];
 #pragma unroll
-  for (int s = 0; s < WMAX; ++s)
-    if (s < w) g[s] = z[c[s]];
+  for (int s = 0; s < W; ++s) g[s] = z[c[s]];
   T acc = T(0);
 #pragma unroll
-  for (int s = 0; s < WMAX; ++s)
-    if (s < w) acc = add_rn(acc, mul_rn(v[s], g[s]));
+  for (int s = 0; s < W; ++s) acc = add_rn(acc, mul_rn(v[s], g[s]));
   z[i] = div_rn(sub_rn(ri, acc), d);
+}
+
+template <typename T>
+using LowerKernel = void (*)(const int32_t*, const T*, int64_t, int64_t, int64_t, const T*, const T*, T*);
+
+template <typename T, int... Ws>
+__host__ LowerKernel<T> lower_kernel_of(int w, std::integer_sequence<int, Ws...>) {
+  LowerKernel<T> tab[] = {k_gs_lower<T, Ws>...};
+  return tab[w];
+}
+// the kernel for width w in [0, 27]
+template <typename T>
+__host__ LowerKernel<T> lower_kernel(int w) {
+  return lower_kernel_of<T>(w, std::make_integer_sequence<int, kWidth + 1>{});
 }
 
 }  // namespace hpg
