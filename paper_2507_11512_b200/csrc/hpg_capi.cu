@@ -220,6 +220,7 @@ struct hpg_ctx {
   char** d_peer = nullptr;
   unsigned int* done = nullptr;
   uint64_t halo_seq = 0, ar_seq = 0;
+  std::vector<std::pair<int, int>> cgs_cfg;  // (kb max, WR*100 + RPW*10 + U)
   int64_t overlap_rows = 1 << 20;  // only levels this large hide an exchange behind interior rows
   ncclComm_t comm = nullptr;
   int nb = 0;                   // reduction grid
@@ -749,6 +750,56 @@ int cgs2_passes(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
 // (h1, h2, beta) to pinned host memory; cgs2_finish waits for it.  Splitting
 // the two lets the host enqueue the next Arnoldi step's V-cycle and SpMV
 // before it blocks on this step's coefficients.
+// (WR, RPW, U) of the fused kernel per basis size: encoded WR*100 + RPW*10 + U
+// (RPW < 10).  HPG_CGS_CFG="kbmax:code,kbmax:code,..." overrides (tuning).
+int cgs_config(hpg_ctx* c, int kb) {
+  if (c->cgs_cfg.empty()) {
+    const char* e = getenv("HPG_CGS_CFG");
+    if (e) {
+      int kbm, code, off = 0, used = 0;
+      while (sscanf(e + off, "%d:%d%n", &kbm, &code, &used) == 2) {
+        c->cgs_cfg.push_back({kbm, code});
+        off += used;
+        if (e[off] == ',') ++off;
+      }
+    }
+    if (c->cgs_cfg.empty())
+      c->cgs_cfg = {{1, 118}, {2, 218}, {4, 418}, {8, 424}, {16, 442}, {24, 461}, {32, 481}, {64, 881}};
+  }
+  for (const auto& e : c->cgs_cfg)  // a configuration must hold all kb rows (WR * RPW >= kb)
+    if (kb <= e.first && (e.second / 100) * ((e.second / 10) % 10) >= kb) return e.second;
+  return 881;
+}
+
+template <typename T>
+int cgs2_fused_dispatch(hpg_ctx* c, int code, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
+  switch (code) {
+#define HPG_CGS_CASE(WR, RPW, U) \
+  case WR * 100 + RPW * 10 + U:  \
+    return cgs2_fused<T, WR, RPW, U>(c, Q, ldq, kb, w, qnext);
+    HPG_CGS_CASE(1, 1, 8)
+    HPG_CGS_CASE(2, 1, 8)
+    HPG_CGS_CASE(4, 1, 8)
+    HPG_CGS_CASE(8, 1, 8)
+    HPG_CGS_CASE(4, 2, 4)
+    HPG_CGS_CASE(8, 2, 4)
+    HPG_CGS_CASE(4, 2, 2)
+    HPG_CGS_CASE(4, 3, 2)
+    HPG_CGS_CASE(8, 3, 2)
+    HPG_CGS_CASE(4, 4, 2)
+    HPG_CGS_CASE(8, 4, 2)
+    HPG_CGS_CASE(4, 4, 1)
+    HPG_CGS_CASE(2, 4, 2)
+    HPG_CGS_CASE(2, 8, 1)
+    HPG_CGS_CASE(4, 6, 1)
+    HPG_CGS_CASE(8, 6, 1)
+    HPG_CGS_CASE(4, 8, 1)
+    HPG_CGS_CASE(8, 8, 1)
+#undef HPG_CGS_CASE
+  }
+  return fail(HPG_E_ARG, "unknown CGS2 configuration %d", code);
+}
+
 template <typename T>
 int cgs2_launch_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext) {
   const int kb = k + 1;
@@ -766,13 +817,7 @@ int cgs2_launch_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext) {
       else if (kb <= 32) rc = cgs2_passes<T, 8, 4, 2>(c, Q, ldq, kb, w, qnext);
       else rc = cgs2_passes<T, 8, 8, 1>(c, Q, ldq, kb, w, qnext);
     } else if ((c->nranks == 1 || c->p2p) && c->cgs_fused && vec_ok) {
-      if (kb <= 1) rc = cgs2_fused<T, 1, 1, 8>(c, Q, ldq, kb, w, qnext);
-      else if (kb <= 2) rc = cgs2_fused<T, 2, 1, 8>(c, Q, ldq, kb, w, qnext);
-      else if (kb <= 4) rc = cgs2_fused<T, 4, 1, 8>(c, Q, ldq, kb, w, qnext);
-      else if (kb <= 8) rc = cgs2_fused<T, 4, 2, 4>(c, Q, ldq, kb, w, qnext);
-      else if (kb <= 16) rc = cgs2_fused<T, 8, 2, 4>(c, Q, ldq, kb, w, qnext);
-      else if (kb <= 32) rc = cgs2_fused<T, 8, 4, 2>(c, Q, ldq, kb, w, qnext);
-      else rc = cgs2_fused<T, 8, 8, 1>(c, Q, ldq, kb, w, qnext);
+      rc = cgs2_fused_dispatch<T>(c, cgs_config(c, kb), Q, ldq, kb, w, qnext);
     } else {
       if (kb <= 4) rc = cgs2_kb<T, 4>(c, Q, ldq, kb, w, qnext);
       else if (kb <= 8) rc = cgs2_kb<T, 8>(c, Q, ldq, kb, w, qnext);

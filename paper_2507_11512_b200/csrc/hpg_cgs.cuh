@@ -83,6 +83,9 @@ struct CgsParams {
   uint64_t seq0;   // sequence number of the first of this call's all-reduces
 };
 
+#ifndef HPG_CGS_PIPE_MIN
+#define HPG_CGS_PIPE_MIN 4  // software-pipeline the passes when RPW >= this
+#endif
 constexpr int kCgsThreads = 256;
 constexpr int kCgsWarps = kCgsThreads / 32;
 
@@ -150,10 +153,11 @@ struct CgsStream {
         const int64_t i = (tb + eg * U + u) * TILE + lane * VN;
 #pragma unroll
         for (int r = 0; r < RPW; ++r) {
-          // rows past kb re-read row 0: finite values that are multiplied by hr = 0
-          // or land in unused accumulators -- no select on loaded data
+          // rows past kb are not loaded (warp-uniform predicate; the register is
+          // pre-zeroed, so no select waits on loaded data)
           const int j = rg + r * WR;
-          q[u][r] = __ldcs((const V*)(p.Q + (j < kb ? j : 0) * p.ldq + i));
+          q[u][r] = V{};
+          if (j < kb) q[u][r] = __ldcs((const V*)(p.Q + j * p.ldq + i));
         }
         if (MODE != 3) wv[u] = __ldcg((const V*)(p.w + i));
       }
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
     T acc[RPW];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) acc[r] = T(0);
-    cgs_pass<T, WR, RPW, U, 0, (RPW >= 4)>(p, nullptr, acc, red);
+    cgs_pass<T, WR, RPW, U, 0, (RPW >= HPG_CGS_PIPE_MIN)>(p, nullptr, acc, red);
     cgs_store_rows<T, WR, RPW>(acc, p.kb, p.partial, sacc);
   }
   grid.sync();
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
     T acc[RPW];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) acc[r] = T(0);
-    cgs_pass<T, WR, RPW, U, 1, (RPW >= 4)>(p, p.scal, acc, red);
+    cgs_pass<T, WR, RPW, U, 1, (RPW >= HPG_CGS_PIPE_MIN)>(p, p.scal, acc, red);
     cgs_store_rows<T, WR, RPW>(acc, p.kb, p.partial, sacc);
   }
   grid.sync();
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
     T acc[RPW];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) acc[r] = T(0);
-    cgs_pass<T, WR, RPW, U, 2, (RPW >= 4)>(p, p.scal + 64, acc, red);
+    cgs_pass<T, WR, RPW, U, 2, (RPW >= HPG_CGS_PIPE_MIN)>(p, p.scal + 64, acc, red);
     cgs_store_rows<T, WR, RPW>(acc, 1, p.partial, sacc);
   }
   if (p.qnext == nullptr) return;
@@ -360,7 +364,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs_onepass(const __grid_con
   T acc[RPW];
 #pragma unroll
   for (int r = 0; r < RPW; ++r) acc[r] = T(0);
-  cgs_pass<T, WR, RPW, U, MODE, (RPW >= 4)>(p, h, acc, red);
+  cgs_pass<T, WR, RPW, U, MODE, (RPW >= HPG_CGS_PIPE_MIN)>(p, h, acc, red);
   cgs_store_rows<T, WR, RPW>(acc, MODE == 2 ? 1 : p.kb, p.partial, sacc);
 }
 
@@ -371,7 +375,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_gemv_combine(const __grid_co
   using V = typename Vec16<T>::V;
   __shared__ V red[WR > 1 ? U * kCgsWarps * 32 : 1];
   T acc[RPW];
-  cgs_pass<T, WR, RPW, U, 3, (RPW >= 4)>(p, p.scal, acc, red);
+  cgs_pass<T, WR, RPW, U, 3, (RPW >= HPG_CGS_PIPE_MIN)>(p, p.scal, acc, red);
 }
 
 }  // namespace hpg

@@ -221,7 +221,8 @@ def test_fused_cgs2_matches_per_pass_kernels(dt, L):
     tdt = torch.float32 if dt == "f32" else torch.float64
     prec = _lib.F32 if dt == "f32" else _lib.F64
     tol = 2e-5 if dt == "f32" else 1e-12
-    for k in (0, 5, 29):
+    # every basis-size boundary of the fused kernel's (WR, RPW, U) table
+    for k in (0, 1, 2, 3, 4, 7, 8, 12, 15, 16, 20, 23, 24, 29):
         outs = []
         for fused in (1, 0):
             ctx.set_option("cgs_fused", fused)

@@ -15,6 +15,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--local", type=int, default=256)
     p.add_argument("--reps", type=int, default=20)
+    p.add_argument("--cgs", default="", help="label: time CGS2 for every k of a restart cycle and exit")
     p.add_argument("--brief", default="", help="label: print only the headline keys on one line")
     a = p.parse_args()
     import torch
@@ -41,6 +42,21 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps * 1e3  # us
 
+    if a.cgs:
+        ws = GmresWorkspace.allocate(n, 30, np.float32, device="cuda")
+        ws.Q.normal_()
+        w = torch.randn(n, device="cuda", dtype=torch.float32)
+        res = np.zeros(64)
+        ts = []
+        for k in range(30):
+            ts.append(timeit(lambda: ctx.call("hpg_cgs2", _lib.F32, _lib.ptr(ws.Q), ws.Q.stride(0), k, _lib.ptr(w),
+                                              _lib.ptr(ws.Q[k + 1]), res.ctypes.data_as(C.POINTER(C.c_double))),
+                             reps=5))
+        byts = [(3 * n * (k + 1) * 4 + 7 * n * 4) for k in range(30)]
+        print(a.cgs, "total_us", round(sum(ts), 1), "eff", round(sum(byts) / sum(ts) / 1e3 / 6553.9, 3),
+              [round(t) for t in ts])
+        hier.close()
+        return
     x32 = torch.randn(ne, device="cuda", dtype=torch.float32)
     y32 = torch.empty(n, device="cuda", dtype=torch.float32)
     r32 = torch.randn(n, device="cuda", dtype=torch.float32)
