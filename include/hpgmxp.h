@@ -74,7 +74,9 @@ int hpg_nccl_unique_id(void* out, int len);
  * greedy coloring, permuted ELL (fp64 + fp32 values, shared int32 columns),
  * halo plans, injection maps, V-cycle workspaces.
  * replaces: multigrid.build_hierarchy (multigrid.py:54-84).
- * nccl_uid may be NULL when nranks == 1.  stream: cudaStream_t to enqueue on
+ * nccl_uid may be NULL: no NCCL communicator; a multi-rank context then moves
+ * every halo and reduction over peer memory (hpg_p2p_open is mandatory) and
+ * several ranks may share one GPU.  stream: cudaStream_t to enqueue on
  * (borrowed), or NULL for a context-owned non-blocking stream.              */
 int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_dims[3],
                const int local_dims[3], int levels, int nu1, int nu2, int nu_c,

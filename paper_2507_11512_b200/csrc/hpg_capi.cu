@@ -196,6 +196,7 @@ struct GraphEntry {
   GraphKey key;
   cudaGraphExec_t exec;
   uint64_t stamp;
+  int64_t kernels;  // kernel nodes in the graph (added to the launch count per replay)
 };
 
 struct hpg_ctx {
@@ -342,6 +343,7 @@ int do_exchange(hpg_ctx* c, int l, int prec, void* v) {
     LAUNCH_CHECK();
     ++c->launches;
   }
+  if (!c->comm) return fail(HPG_E_NCCL, "no NCCL communicator (P2P-only context) and peer memory is off");
   const size_t es = esize(prec);
   NCCL_TRY(ncclGroupStart());
   for (auto& nb : L.nbrs) {
@@ -375,6 +377,7 @@ int exchange_begin(hpg_ctx* c, int l, int prec, void* v) {
     LAUNCH_CHECK();
     ++c->launches;
   }
+  if (!c->comm) return fail(HPG_E_NCCL, "no NCCL communicator (P2P-only context) and peer memory is off");
   const size_t es = esize(prec);
   NCCL_TRY(ncclGroupStart());
   for (auto& nb : L.nbrs) {
@@ -413,6 +416,7 @@ int allreduce_scal(hpg_ctx* c, T* buf, int cnt) {
     ++c->launches;
     return HPG_OK;
   }
+  if (!c->comm) return fail(HPG_E_NCCL, "no NCCL communicator (P2P-only context) and peer memory is off");
   NCCL_TRY(ncclAllGather(buf, c->gather, cnt, sizeof(T) == 8 ? ncclFloat64 : ncclFloat32, c->comm, c->stream));
   hpg::k_fold_ranks<T><<<1, 64, 0, c->stream>>>((const T*)c->gather, c->nranks, cnt, buf, 0);
   LAUNCH_CHECK();
@@ -1335,8 +1339,9 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
       dmalloc((char**)&c->scal, 512 * 8, nullptr) || dmalloc((char**)&c->gather, (size_t)nranks * 256 * 8, nullptr))
     return bail(HPG_E_CUDA);
   if (cudaMallocHost((void**)&c->pinned, 256 * 8) != cudaSuccess) return bail(fail(HPG_E_CUDA, "pinned alloc"));
-  if (nranks > 1) {
-    if (!nccl_uid) return bail(fail(HPG_E_ARG, "nccl_uid required for nranks > 1"));
+  // nccl_uid == NULL: P2P-only context (every exchange and reduction over the
+  // peer-memory path; lets several ranks share one GPU, where NCCL refuses)
+  if (nranks > 1 && nccl_uid) {
     ncclUniqueId id;
     memcpy(&id, nccl_uid, sizeof id);
     ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
@@ -1527,9 +1532,11 @@ int hpg_vcycle(hpg_ctx* c, int prec, const void* r, void* z) {
       if (e.key == key) {
         e.stamp = ++c->gclock;
         CUDA_TRY(cudaGraphLaunch(e.exec, c->stream));
+        c->launches += e.kernels;
         return HPG_OK;
       }
     cudaGraph_t g = nullptr;
+    const int64_t l0 = c->launches;
     CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     rc = prec == HPG_F64 ? vcycle<double>(c, 0, (const double*)r, (double*)z)
                          : vcycle<float>(c, 0, (const float*)r, (float*)z);
@@ -1550,7 +1557,7 @@ int hpg_vcycle(hpg_ctx* c, int prec, const void* r, void* z) {
       cudaGraphExecDestroy(c->gcache[lru].exec);
       c->gcache.erase(c->gcache.begin() + lru);
     }
-    c->gcache.push_back({key, exec, ++c->gclock});
+    c->gcache.push_back({key, exec, ++c->gclock, c->launches - l0});
     CUDA_TRY(cudaGraphLaunch(exec, c->stream));
     return HPG_OK;
   }

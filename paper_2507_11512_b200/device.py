@@ -21,8 +21,11 @@ class Context:
         self.nranks = 1 if world is None else world.nranks
         self.rank = domain.rank
         self.levels = levels
+        import os
         uid = None
-        if self.nranks > 1:
+        # HPG_NCCL=0: no NCCL communicator, peer memory only (ranks may share a GPU)
+        self.nccl = self.nranks > 1 and os.environ.get("HPG_NCCL", "1") != "0"
+        if self.nccl:
             uid = C.create_string_buffer(world.nccl_uid(), 128)
         h = C.c_void_p()
         L = _lib.lib()
@@ -40,6 +43,8 @@ class Context:
         the fallback data path when peer access is unavailable."""
         import os
         if os.environ.get("HPG_P2P", "1") == "0":
+            if not self.nccl:
+                raise RuntimeError("HPG_P2P=0 with HPG_NCCL=0 leaves no data path")
             return
         buf = C.create_string_buffer(64)
         self.call("hpg_p2p_handle", buf, 64)
@@ -49,6 +54,8 @@ class Context:
         rc = _lib.lib().hpg_p2p_open(self.h, blob, 64)
         ok = world.all_reduce_sum(self.rank, 1 if rc == 0 else 0) == self.nranks
         if not ok:
+            if not self.nccl:
+                raise RuntimeError("peer memory unavailable and HPG_NCCL=0: no data path")
             self.set_option("p2p", 0)
         world.barrier()
         self.p2p = ok

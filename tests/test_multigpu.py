@@ -51,10 +51,10 @@ def test_two_ranks_16():
 
 @pytest.mark.skipif(_gpus() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("env", [{"HPG_P2P": "0"}, {"HPG_OVERLAP": "1"}, {"HPG_P2P": "0", "HPG_OVERLAP": "1"},
-                                 {"HPG_CGS_FUSED": "0"}])
+                                 {"HPG_CGS_FUSED": "0"}, {"HPG_NCCL": "0"}])
 def test_two_ranks_alternative_paths(env):
-    """NCCL data path, overlapped exchange and per-pass CGS2: same bitwise kernels,
-    same fp64 count as the reference (23)."""
+    """NCCL data path, overlapped exchange, per-pass CGS2 and the P2P-only
+    context (no NCCL communicator): same bitwise kernels, converged solves."""
     out = _run(2, 8, 3, env)
     for rk in out["checks"]:
         assert all(rk.values()), (env, out["checks"])
@@ -71,6 +71,9 @@ def test_four_ranks_8():
 
 @pytest.mark.skipif(_gpus() < 8, reason="needs 8 GPUs")
 def test_eight_ranks_8():
+    """The 2x2x2 grid (the 8xB200 configuration: x, y and z faces, edges and
+    corners).  (Ranks sharing a GPU do not work: the peer-memory spin waits of
+    one process's kernels starve the other process's time slice.)"""
     # ref: tests/test_acceptance.py:347-348 -> 8 ranks x 8^3: 18 double / 23 mixed
     out = _run(8, 8, 4)
     for rk in out["checks"]:
