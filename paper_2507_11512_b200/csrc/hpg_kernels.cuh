@@ -112,50 +112,6 @@ __device__ __forceinline__ T ldv(const T* p) {
   return *p;
 }
 
-// HPG_Z_HINT: the gathered vector (the smoother's z, the SpMV's x) is marked
-// evict-last in L2 so that it survives the gigabytes of matrix planes streaming
-// past it between color passes (1: fp32 only, 2: fp32 and fp64).
-#ifndef HPG_Z_HINT
-#define HPG_Z_HINT 0
-#endif
-template <typename T>
-__device__ __forceinline__ bool z_hint() {
-  return HPG_Z_HINT == 2 || (HPG_Z_HINT == 1 && sizeof(T) == 4);
-}
-__device__ __forceinline__ uint64_t keep_policy() {
-  uint64_t pol = 0;
-#if HPG_Z_HINT
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-#endif
-  return pol;
-}
-__device__ __forceinline__ float ld_keep(const float* p, uint64_t pol) {
-  float v;
-  asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
-  double v;
-  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void st_keep(float* p, float v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
-template <bool COHERENT, typename T>
-__device__ __forceinline__ T ldg_vec(const T* p) {
-  if (!COHERENT && z_hint<T>()) return ld_keep(p, keep_policy());
-  return ldv<COHERENT>(p);
-}
-template <typename T>
-__device__ __forceinline__ void st_vec(T* p, T v) {
-  if (z_hint<T>()) st_keep(p, v, keep_policy());
-  else *p = v;
-}
-
 // known0 >= 0: columns >= known0 are known to hold 0 (the smoother's zero
 // initial guess for colors not yet updated in this sweep, and the zeroed halo):
 // their products are still formed -- v * 0, the reference's arithmetic -- only
@@ -182,7 +138,7 @@ __device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, co
 #pragma unroll
   for (int s = 0; s < 27; ++s) {
     const int32_t cc = c[s] < 0 ? ~c[s] : c[s];
-    g[s] = (known0 >= 0 && cc >= known0) ? T(0) : ldg_vec<COHERENT>(x + cc);
+    g[s] = (known0 >= 0 && cc >= known0) ? T(0) : ldv<COHERENT>(x + cc);
   }
   T acc = T(0);
 #pragma unroll
@@ -249,9 +205,7 @@ __device__ __forceinline__ void gs_row(const int32_t* __restrict__ cols, const T
                                        int64_t i, const T* __restrict__ r, T* z, int64_t known0 = -1) {
   T d = T(0);
   const T acc = row_accumulate<T, true, COHERENT, PDL>(cols, vals, ld, i, z, &d, known0);
-  const T zi = div_rn(sub_rn(ldv<COHERENT>(r + i), acc), d);
-  if (COHERENT) z[i] = zi;
-  else st_vec(z + i, zi);
+  z[i] = div_rn(sub_rn(ldv<COHERENT>(r + i), acc), d);
 }
 
 // SPLIT: rows may be skipped (skip[i] != 0) or taken from a list (interior /

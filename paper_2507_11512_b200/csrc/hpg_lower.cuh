@@ -119,11 +119,11 @@ __global__ void __launch_bounds__(256, lower_minb<T, W>()) k_gs_lower(const int3
   const T ri = r[i];
   T g[W > 0 ? W : 1];
 #pragma unroll
-  for (int s = 0; s < W; ++s) g[s] = ldg_vec<false>(z + c[s]);
+  for (int s = 0; s < W; ++s) g[s] = z[c[s]];
   T acc = T(0);
 #pragma unroll
   for (int s = 0; s < W; ++s) acc = add_rn(acc, mul_rn(v[s], g[s]));
-  st_vec(z + i, div_rn(sub_rn(ri, acc), d));
+  z[i] = div_rn(sub_rn(ri, acc), d);
 }
 
 template <typename T>
