@@ -156,6 +156,8 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
 /* Tuning switches (results are identical up to reduction order):
  *   "cgs_fused"  1: single-rank CGS2 as one cooperative bulk-copy kernel, 0: per-pass kernels
  *   "tail_rows"  levels with at most this many rows run in the persistent V-cycle tail kernel
+ *   "tail_cluster" > 0: that tail kernel runs as ONE cluster of this many CTAs (<= 16,
+ *                hardware cluster barrier); 0: a cooperative grid (grid-wide barrier)
  *   "pdl"        1: stencil kernels use programmatic dependent launch
  *   "overlap"    1: multi-rank SpMV / GS overlap the halo exchange with interior rows
  *   "overlap_rows" only levels with at least this many rows overlap (default 2^20)
@@ -163,6 +165,7 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
  *   "graphs"     1: single-rank V-cycles replay a captured CUDA graph per (prec, r, z)
  *   "known_zero" 1: zero-initial-guess sweeps skip the loads of not-yet-updated colors
  *   "gs_minb"    blocks per SM the color-pass kernel is compiled for (2 or 3)
+ *   "gs_rev"     1: odd colors' passes walk their block backwards (L2 reuse at the turn)
  *   "wave"       bit mask (1 fp64, 2 fp32): forward sweeps as one dataflow kernel
  *                (bitwise identical; default 1) */
 int hpg_set_option(hpg_ctx* ctx, const char* key, int64_t value);

@@ -248,8 +248,10 @@ struct hpg_ctx {
   uint64_t gclock = 0;
   bool pdl = true;
   int gs_minb = 3;
+  bool gs_rev = true;   // odd colors walk their block backwards (L2 reuse of z at the turn)
   int64_t tail_rows = 0;        // levels with n <= tail_rows run in the persistent tail kernel
   int tail_blocks[2] = {0, 0};  // cooperative grid (f64, f32)
+  int tail_cluster = 0;         // > 0: run the tail as one cluster of this many CTAs
   // per-motif CUDA-event timers (ref: metrics.py:125-131 Tally.timed)
   bool timing = false;
   std::vector<cudaEvent_t> events;
@@ -426,20 +428,20 @@ int allreduce_scal(hpg_ctx* c, T* buf, int cnt) {
 
 template <typename T>
 int gs_pass_launch(hpg_ctx* c, Level& L, int64_t a, int64_t cnt, const T* r, T* z, const uint8_t* skip,
-                   const int32_t* list, int64_t known0 = -1) {
+                   const int32_t* list, int64_t known0 = -1, int rev = 0) {
   const T* vals = vals_of<T>(L);
   if (skip || list)
     CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3, true>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip,
-                        list, known0));
+                        list, known0, 0));
   else if (c->gs_minb == 3)
     CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
-                        known0));
+                        known0, rev));
   else if (c->gs_minb == 4)
     CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 4>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
-                        known0));
+                        known0, rev));
   else
     CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 2>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
-                        known0));
+                        known0, rev));
   ++c->launches;
   return HPG_OK;
 }
@@ -452,7 +454,9 @@ int gs_lower_launch(hpg_ctx* c, Level& L, int col, const T* r, T* z) {
   const int32_t* lcols = L.lcols + lc.base;
   const T* lv = (sizeof(T) == 8 ? (const T*)L.lv64 : (const T*)L.lv32) + lc.base;
   const T* dg = sizeof(T) == 8 ? (const T*)L.dg64 : (const T*)L.dg32;
-  cudaError_t e = launch_pdl(c, hpg::lower_kernel<T>(lc.w), grid_for(cnt), 256, lcols, lv, lc.ldc, a, cnt, dg, r, z);
+  const int rev = c->gs_rev && (col & 1);
+  cudaError_t e =
+      launch_pdl(c, hpg::lower_kernel<T>(lc.w), grid_for(cnt), 256, lcols, lv, lc.ldc, a, cnt, dg, r, z, rev);
   CUDA_TRY(e);
   ++c->launches;
   return HPG_OK;
@@ -525,7 +529,8 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
       CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n_ext - L.n, 4)), 256, z + L.n, L.n_ext - L.n));
     for (int col = 0; col < L.g.ncolors; ++col) {
       const int64_t a = L.g.off[col], b = L.g.off[col + 1];
-      if (b > a && (rc = gs_pass_launch<T>(c, L, a, b - a, r, z, nullptr, nullptr, a))) return rc;
+      if (b > a && (rc = gs_pass_launch<T>(c, L, a, b - a, r, z, nullptr, nullptr, a, c->gs_rev && (col & 1))))
+        return rc;
     }
     return HPG_OK;
   }
@@ -545,7 +550,7 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
   for (int col = first; col < L.g.ncolors; ++col) {
     const int64_t a = L.g.off[col], b = L.g.off[col + 1];
     if (b <= a) continue;
-    if ((rc = gs_pass_launch<T>(c, L, a, b - a, r, z, nullptr, nullptr))) return rc;
+    if ((rc = gs_pass_launch<T>(c, L, a, b - a, r, z, nullptr, nullptr, -1, c->gs_rev && (col & 1)))) return rc;
   }
   return HPG_OK;
 }
@@ -613,12 +618,36 @@ int vcycle_tail(hpg_ctx* c, int l, const T* r, T* z) {
     for (int q = 0; q < 9; ++q) t.off[q] = L.g.off[q];
     t.ncolors = L.g.ncolors;
   }
-  const int blocks = c->tail_blocks[sizeof(T) == 4];
-  void* args[] = {(void*)&p};
-  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)hpg::k_vcycle_tail<T>, dim3(blocks), dim3(256), args, 0,
-                                       c->stream));
+  if (c->tail_cluster > 0) {
+    // the whole tail on ONE thread-block cluster (hardware cluster barrier)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->tail_cluster);
+    cfg.blockDim = dim3(256);
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c->tail_cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, hpg::k_vcycle_tail<T, true>, p));
+  } else {
+    const int blocks = c->tail_blocks[sizeof(T) == 4];
+    void* args[] = {(void*)&p};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)hpg::k_vcycle_tail<T, false>, dim3(blocks), dim3(256), args,
+                                         0, c->stream));
+  }
   ++c->launches;
   return HPG_OK;
+}
+
+void set_tail_cluster(hpg_ctx* c, int v) {
+  c->tail_cluster = std::max(0, std::min(v, 16));
+  if (c->tail_cluster > 8) {  // non-portable cluster sizes (up to 16) must be opted into
+    cudaFuncSetAttribute(hpg::k_vcycle_tail<double, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(hpg::k_vcycle_tail<float, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }
 }
 
 // V-cycle with zero initial guess (ref: multigrid.py:140-171)
@@ -1309,6 +1338,8 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     c->wave_blocks[1] = std::min(occ(wave_fn<float>(true)), occ(wave_fn<float>(false)));
     const char* f = getenv("HPG_CGS_FUSED");
     c->cgs_fused = !(f && f[0] == '0');
+    const char* rv = getenv("HPG_GS_REV");
+    if (rv) c->gs_rev = rv[0] != '0';
     const char* mb = getenv("HPG_GS_MINB");
     if (mb) c->gs_minb = atoi(mb);
     const char* lw = getenv("HPG_LOWER");
@@ -1326,10 +1357,12 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     const char* g = getenv("HPG_PDL");
     c->pdl = !(g && g[0] == '0');
     int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hpg::k_vcycle_tail<double>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hpg::k_vcycle_tail<double, false>, 256, 0);
     c->tail_blocks[0] = std::max(1, per) * sms;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hpg::k_vcycle_tail<float>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, hpg::k_vcycle_tail<float, false>, 256, 0);
     c->tail_blocks[1] = std::max(1, per) * sms;
+    const char* tc = getenv("HPG_TAIL_CLUSTER");
+    if (tc) set_tail_cluster(c, atoi(tc));
   }
   c->nb = (int)std::min<int64_t>(8 * sms, std::max<int64_t>(1, cdiv(c->lev[0].n, 256)));
   c->spmv_partial_len = grid_for(c->lev[0].n);
@@ -1772,6 +1805,8 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
     c->gcache.clear();
   }
   else if (!strcmp(key, "tail_rows")) c->tail_rows = value;
+  else if (!strcmp(key, "tail_cluster")) set_tail_cluster(c, (int)value);
+  else if (!strcmp(key, "gs_rev")) c->gs_rev = value != 0;
   else return fail(HPG_E_ARG, "unknown option %s", key);
   return HPG_OK;
 }

@@ -93,6 +93,15 @@ constexpr int lower_minb() {
                         : (W <= 4 ? 6 : W <= 8 ? 5 : W <= 12 ? 4 : W <= 16 ? 3 : 2);
 }
 
+// L2 evict-first hint on the lower-part planes (1: fp32 sweeps, 2: fp32 and fp64)
+#ifndef HPG_LOWER_HINT
+#define HPG_LOWER_HINT 1
+#endif
+template <typename T>
+__device__ __forceinline__ constexpr bool lower_hint() {
+  return HPG_LOWER_HINT == 2 || (HPG_LOWER_HINT == 1 && sizeof(T) == 4);
+}
+
 // One color of the zero-initial-guess sweep: z_i = (r_i - sum_lower v z) / a_ii,
 // instantiated per exact width W (no predicated slots).
 template <typename T, int W>
@@ -100,18 +109,27 @@ __global__ void __launch_bounds__(256, lower_minb<T, W>()) k_gs_lower(const int3
                                                                        const T* __restrict__ lvals, int64_t ldc,
                                                                        int64_t row0, int64_t nrows,
                                                                        const T* __restrict__ dg,
-                                                                       const T* __restrict__ r, T* z) {
+                                                                       const T* __restrict__ r, T* z, int rev) {
   pdl_trigger();
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t blk = rev ? (int64_t)(gridDim.x - 1 - blockIdx.x) : (int64_t)blockIdx.x;  // see k_gs_pass
+  const int64_t j = blk * blockDim.x + threadIdx.x;
   if (j >= nrows) return;
   const int64_t i = row0 + j;
-  const uint64_t pol = stream_policy();
   int32_t c[W > 0 ? W : 1];
   T v[W > 0 ? W : 1];
+  if (lower_hint<T>()) {  // evict-first: keep z (gathered by every color) in L2
+    const uint64_t pol = evict_first_policy();
 #pragma unroll
-  for (int s = 0; s < W; ++s) c[s] = ld_stream(lcols + s * ldc + j, pol);
+    for (int s = 0; s < W; ++s) c[s] = ld_stream_ef(lcols + s * ldc + j, pol);
 #pragma unroll
-  for (int s = 0; s < W; ++s) v[s] = ld_stream(lvals + s * ldc + j, pol);
+    for (int s = 0; s < W; ++s) v[s] = ld_stream_ef(lvals + s * ldc + j, pol);
+  } else {
+    const uint64_t pol = stream_policy();
+#pragma unroll
+    for (int s = 0; s < W; ++s) c[s] = ld_stream(lcols + s * ldc + j, pol);
+#pragma unroll
+    for (int s = 0; s < W; ++s) v[s] = ld_stream(lvals + s * ldc + j, pol);
+  }
   const T d = dg[i];
   // z of the earlier colors (and r) are written by previous kernels
   if (W > 0) pdl_wait_after(v[0]);
@@ -127,7 +145,7 @@ __global__ void __launch_bounds__(256, lower_minb<T, W>()) k_gs_lower(const int3
 }
 
 template <typename T>
-using LowerKernel = void (*)(const int32_t*, const T*, int64_t, int64_t, int64_t, const T*, const T*, T*);
+using LowerKernel = void (*)(const int32_t*, const T*, int64_t, int64_t, int64_t, const T*, const T*, T*, int);
 
 template <typename T, int... Ws>
 __host__ LowerKernel<T> lower_kernel_of(int w, std::integer_sequence<int, Ws...>) {

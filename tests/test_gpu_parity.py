@@ -300,7 +300,8 @@ def test_nonuniform_boxes_vcycle_bitwise_vs_oracle(dims):
 
 
 def test_execution_variants_agree_bitwise():
-    """Tuning switches never change results: the persistent V-cycle tail kernel,
+    """Tuning switches never change results: the persistent V-cycle tail kernel
+    (cooperative grid, or one 16- / 8-CTA cluster), backwards odd-color passes,
     CUDA-graph replay, PDL, the known-zero sweep, the dataflow (wave) sweep and
     the strictly-lower zero sweep give the same V-cycle bits in both precisions; the host-pipelined and plain
     Arnoldi loops give the same iterations and solution."""
@@ -313,7 +314,7 @@ def test_execution_variants_agree_bitwise():
     rs = [torch.randn(h.levels[0].A_hi.n_rows, device="cuda", dtype=dt,
                       generator=torch.Generator("cuda").manual_seed(3)) for dt in (torch.float32, torch.float64)]
     refs = [h.apply(r).cpu().numpy() for r in rs]
-    for key, val in (("tail_rows", 1 << 30), ("graphs", 0), ("pdl", 0), ("known_zero", 0), ("wave", 0),
+    for key, val in (("tail_rows", 1 << 30), ("tail_cluster", 16), ("tail_cluster", 8), ("gs_rev", 1), ("graphs", 0), ("pdl", 0), ("known_zero", 0), ("wave", 0),
                      ("lower", 0)):
         ctx.set_option(key, val)
         for r, ref in zip(rs, refs):
@@ -323,6 +324,8 @@ def test_execution_variants_agree_bitwise():
     ctx.set_option("wave", 1)
     ctx.set_option("lower", 1)
     ctx.set_option("tail_rows", 0)
+    ctx.set_option("tail_cluster", 0)
+    ctx.set_option("gs_rev", 0)
     ctx.set_option("graphs", 1)
     ctx.set_option("pdl", 1)
     lv = h.levels[0]

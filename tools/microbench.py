@@ -140,7 +140,8 @@ def main():
     out["solve30_motif_s"] = tal.seconds
     if a.brief:
         keys = ("gs_sweep_L0_f32_us", "gs_sweep0_L0_f32_us", "zero_sweep_slots_per_row", "gs_sweep_L0_f64_us", "vcycle_f32_us", "vcycle_f64_us", "spmv_f32_us",
-                "cgs2_k30_us", "solve30_ms")
+                "cgs2_k30_us", "solve30_ms", "gs_sweep_L1_f32_us", "gs_sweep0_L1_f32_us", "gs_sweep_L2_f32_us",
+                "gs_sweep0_L2_f32_us", "gs_sweep_L3_f32_us", "gs_sweep0_L3_f32_us")
         print(a.brief, {k: round(v, 1) for k, v in out.items() if k in keys})
     else:
         print(json.dumps(out))
