@@ -33,6 +33,36 @@ def main():
         e1.record(ctx.stream)
         torch.cuda.synchronize()
         out[f"exchange_L{li}_us"] = round(e0.elapsed_time(e1) / 50 * 1e3, 2)
+    # level-0 kernels that carry a collective: CGS2 (3 all-reduces), SpMV and a
+    # GS sweep (one exchange each), back to back
+    import numpy as np
+    from paper_2507_11512_b200.krylov import GmresWorkspace
+    lv = h.levels[0]
+    n, ne = lv.A_hi.n_rows, lv.A_hi.n_cols_extended
+    ws = GmresWorkspace.allocate(n, 30, np.float32, device="cuda")
+    ws.Q.normal_()
+    w = torch.randn(-(-n // 32) * 32, device="cuda")[:n]
+    res = np.zeros(64)
+    x = torch.randn(ne, device="cuda")
+    y = torch.empty(n, device="cuda")
+
+    def timeit(fn, reps=10):
+        fn()
+        torch.cuda.synchronize()
+        world.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream)
+        for _ in range(reps):
+            fn()
+        e1.record(ctx.stream)
+        torch.cuda.synchronize()
+        return round(e0.elapsed_time(e1) / reps * 1e3, 1)
+    for k in (0, 15, 29):
+        out[f"cgs2_kb{k + 1}_us"] = timeit(lambda: ctx.call(
+            "hpg_cgs2", _lib.F32, _lib.ptr(ws.Q), ws.Q.stride(0), k, _lib.ptr(w), _lib.ptr(ws.Q[k + 1]),
+            res.ctypes.data_as(C.POINTER(C.c_double))))
+    out["spmv_L0_us"] = timeit(lambda: ctx.call("hpg_spmv", 0, _lib.F32, _lib.ptr(x), _lib.ptr(y)))
+    out["gs_sweep_L0_us"] = timeit(lambda: ctx.call("hpg_gs_sweep", 0, _lib.F32, _lib.ptr(y), _lib.ptr(x), 0))
     vals = (C.c_double * 4)(1, 2, 3, 4)
     world.barrier()
     import time
