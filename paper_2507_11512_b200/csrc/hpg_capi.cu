@@ -155,6 +155,8 @@ struct Level {
   int32_t* f2c = nullptr;  // (coarse levels, general colorings) fine row of coarse row i
   int32_t* perm_d = nullptr;   // general coloring tables (null: greedy closed form)
   int32_t* iperm_d = nullptr;
+  hpg::Stencil st{};           // implicit-index rows (st.on when the layout allows, checked at build)
+  int64_t st_rows = 0;         // rows that skip their column-index loads
   hpg::WaveLevel wave;         // dataflow sweep plan (valid when wave_ok)
   bool wave_ok = false;
   int32_t* wave_items = nullptr;
@@ -249,6 +251,7 @@ struct hpg_ctx {
   bool pdl = true;
   int gs_minb = 3;
   bool gs_rev = true;   // odd colors walk their block backwards (L2 reuse of z at the turn)
+  bool stencil = true;  // interior rows compute their ELL columns instead of loading them
   int64_t tail_rows = 0;        // levels with n <= tail_rows run in the persistent tail kernel
   int tail_blocks[2] = {0, 0};  // cooperative grid (f64, f32)
   int tail_cluster = 0;         // > 0: run the tail as one cluster of this many CTAs
@@ -292,6 +295,8 @@ template <>
 double* vals_of<double>(const Level& L) { return L.v64; }
 template <>
 float* vals_of<float>(const Level& L) { return L.v32; }
+
+hpg::Stencil stencil_of(const hpg_ctx* c, const Level& L) { return c->stencil ? L.st : hpg::Stencil{}; }
 
 int grid_for(int64_t n, int threads = 256) { return (int)std::max<int64_t>(1, cdiv(n, threads)); }
 
@@ -432,16 +437,16 @@ int gs_pass_launch(hpg_ctx* c, Level& L, int64_t a, int64_t cnt, const T* r, T* 
   const T* vals = vals_of<T>(L);
   if (skip || list)
     CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3, true>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip,
-                        list, known0, 0));
+                        list, known0, 0, stencil_of(c, L)));
   else if (c->gs_minb == 3)
     CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
-                        known0, rev));
+                        known0, rev, stencil_of(c, L)));
   else if (c->gs_minb == 4)
     CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 4>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
-                        known0, rev));
+                        known0, rev, stencil_of(c, L)));
   else
     CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 2>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
-                        known0, rev));
+                        known0, rev, stencil_of(c, L)));
   ++c->launches;
   return HPG_OK;
 }
@@ -565,7 +570,7 @@ int restrict_(hpg_ctx* c, int l, const T* rf, const T* zf, T* rcoarse) {
                         (const int32_t*)C.f2c, rf, zf, rcoarse));
   else
     CUDA_TRY(launch_pdl(c, hpg::k_restrict<T>, grid_for(C.n), 256, F.cols, (const T*)vals_of<T>(F), F.ld, C.n,
-                        (const int32_t*)C.inj, rf, zf, rcoarse));
+                        (const int32_t*)C.inj, rf, zf, rcoarse, stencil_of(c, F)));
   ++c->launches;
   return HPG_OK;
 }
@@ -993,6 +998,53 @@ int build_lower(hpg_ctx* c, Level& L) {
   return HPG_OK;
 }
 
+// Implicit-index rows (hpg_kernels.cuh Stencil): eligible for the greedy
+// layout with even local extents (8 equal color blocks); every row that takes
+// the closed form is compared with its stored ELL columns, and any mismatch
+// leaves the level on the index stream.
+int build_stencil(hpg_ctx* c, Level& L) {
+  L.st = hpg::Stencil{};
+  L.st_rows = 0;
+  const Geom& g = L.g;
+  if (!L.n || g.perm_tab || g.ncolors != 8 || ((g.lx | g.ly | g.lz) & 1) || g.lx < 2 || g.ly < 2 || g.lz < 2 ||
+      L.n >= (int64_t{1} << 31))
+    return HPG_OK;
+  const int64_t n8 = L.n / 8;
+  for (int k = 0; k <= 8; ++k)
+    if (g.off[k] != k * n8) return HPG_OK;
+  hpg::Stencil st{};
+  st.on = 1;
+  st.n8 = (uint32_t)n8;
+  st.hx = (uint32_t)(g.lx / 2);
+  st.hy = (uint32_t)(g.ly / 2);
+  st.hxy = st.hx * st.hy;
+  st.lx = g.lx;
+  st.ly = g.ly;
+  st.lz = g.lz;
+  st.bx = g.bit[0];
+  st.by = g.bit[1];
+  st.bz = g.bit[2];
+  st.cx = st.n8 << st.bx;
+  st.cy = st.n8 << st.by;
+  st.cz = st.n8 << st.bz;
+  void* scratch = nullptr;
+  CUDA_TRY(cudaMalloc(&scratch, 16));
+  CUDA_TRY(cudaMemsetAsync(scratch, 0, 16, c->stream));
+  unsigned long long* rows = (unsigned long long*)scratch;
+  unsigned int* bad = (unsigned int*)((char*)scratch + 8);
+  hpg::k_check_stencil<<<grid_for(L.n), 256, 0, c->stream>>>(L.cols, L.ld, L.n, st, bad, rows);
+  LAUNCH_CHECK();
+  unsigned long long h[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(h, scratch, 16, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  cudaFree(scratch);
+  if ((unsigned int)h[1] == 0) {
+    L.st = st;
+    L.st_rows = (int64_t)h[0];
+  }
+  return HPG_OK;
+}
+
 // (Re)build a level's permutation-dependent structure: ELL rows, send lists and
 // the interior/boundary split.  `first` allocates the send/split buffers.
 int build_structure(hpg_ctx* c, Level& L, bool first) {
@@ -1001,6 +1053,7 @@ int build_structure(hpg_ctx* c, Level& L, bool first) {
     hpg::k_build_level<<<grid_for(L.n, 128), 128, 0, c->stream>>>(L.g, L.ld, L.cols, L.v64, L.v32);
     LAUNCH_CHECK();
     if ((rc = build_lower(c, L))) return rc;
+    if ((rc = build_stencil(c, L))) return rc;
   }
   // halo plan: one send list per neighbour, in ascending neighbour rank
   struct Tmp {
@@ -1137,10 +1190,11 @@ int spmv_launch(hpg_ctx* c, Level& L, int64_t cnt, const T* x, T* y, const uint8
   if (skip || list)
     CUDA_TRY(launch_pdl(c, hpg::k_spmv<T, 0, true>, grid_for(cnt), 256, (const int32_t*)L.cols,
                         (const T*)vals_of<T>(L), L.ld, (int64_t)0, cnt, x, (const T*)nullptr, y, (double*)nullptr,
-                        skip, list));
+                        skip, list, stencil_of(c, L)));
   else
     CUDA_TRY(launch_pdl(c, hpg::k_spmv<T, 0>, grid_for(cnt), 256, (const int32_t*)L.cols, (const T*)vals_of<T>(L),
-                        L.ld, (int64_t)0, cnt, x, (const T*)nullptr, y, (double*)nullptr, skip, list));
+                        L.ld, (int64_t)0, cnt, x, (const T*)nullptr, y, (double*)nullptr, skip, list,
+                        stencil_of(c, L)));
   ++c->launches;
   return HPG_OK;
 }
@@ -1338,6 +1392,8 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     c->wave_blocks[1] = std::min(occ(wave_fn<float>(true)), occ(wave_fn<float>(false)));
     const char* f = getenv("HPG_CGS_FUSED");
     c->cgs_fused = !(f && f[0] == '0');
+    const char* sn = getenv("HPG_STENCIL");
+    if (sn) c->stencil = sn[0] != '0';
     const char* rv = getenv("HPG_GS_REV");
     if (rv) c->gs_rev = rv[0] != '0';
     const char* mb = getenv("HPG_GS_MINB");
@@ -1428,7 +1484,8 @@ int hpg_level_info(hpg_ctx* c, int l, int64_t* info, int ninfo) {
   for (int k = 0; k < L.g.ncolors; ++k)
     ls += (L.lower_ok ? L.lc[k].w : hpg::kWidth) * (L.g.off[k + 1] - L.g.off[k]);
   tmp[17] = ls;
-  for (int k = 0; k < ninfo && k < 18; ++k) info[k] = tmp[k];
+  tmp[18] = L.st.on ? L.st_rows : 0;  // rows on the implicit-index path
+  for (int k = 0; k < ninfo && k < 19; ++k) info[k] = tmp[k];
   return HPG_OK;
 }
 
@@ -1650,7 +1707,7 @@ int hpg_residual(hpg_ctx* c, const double* b, double* x, double* r, double* rho2
   double* scal = (double*)c->scal;
   const int nbk = grid_for(L.n);
   hpg::k_spmv<double, 1><<<nbk, 256, 0, c->stream>>>(L.cols, L.v64, L.ld, 0, L.n, x, b, r, c->spmv_partial, nullptr,
-                                                     nullptr);
+                                                     nullptr, stencil_of(c, L));
   hpg::k_fold<double><<<1, 1024, 0, c->stream>>>(c->spmv_partial, nbk, 1, scal + 200, 0);
   LAUNCH_CHECK();
   c->launches += 2;
@@ -1807,6 +1864,11 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   else if (!strcmp(key, "tail_rows")) c->tail_rows = value;
   else if (!strcmp(key, "tail_cluster")) set_tail_cluster(c, (int)value);
   else if (!strcmp(key, "gs_rev")) c->gs_rev = value != 0;
+  else if (!strcmp(key, "stencil")) {
+    c->stencil = value != 0;
+    for (auto& e : c->gcache) cudaGraphExecDestroy(e.exec);  // captured launches carry the old arguments
+    c->gcache.clear();
+  }
   else return fail(HPG_E_ARG, "unknown option %s", key);
   return HPG_OK;
 }

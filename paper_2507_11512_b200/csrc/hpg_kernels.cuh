@@ -135,18 +135,64 @@ __device__ __forceinline__ T ldv(const T* p) {
   return *p;
 }
 
+// Implicit-index ("stencil layout") rows.  With the greedy coloring and even
+// local extents every color block is an (lx/2)(ly/2)(lz/2) sub-lattice of the
+// same size n8 (ref: coloring.py:78-80 order), and a row whose 27 neighbours
+// all lie inside the local box has its ELL columns in closed form: slot s is
+// offset (dx,dy,dz) in z-slowest order (problem.py:88-142 compaction keeps all
+// 27), column = color(x+dx, y+dy, z+dz) * n8 + natural position in that
+// sub-lattice.  Such rows skip the 27 column-index loads -- 4 of the 8 (fp32)
+// or 12 (fp64) bytes per nonzero -- and gather exactly the columns stored in
+// the ELL (checked row by row at build, k_check_stencil), so sums are bitwise
+// unchanged.  Rows on a face of the box stream their ELL columns as before.
+struct Stencil {
+  int on;
+  uint32_t n8, hx, hy, hxy;  // color block size; sub-lattice extents
+  uint32_t cx, cy, cz;       // color-block offset contributed by an odd x / y / z
+  int lx, ly, lz;
+  int bx, by, bz;            // parity bit of each axis in the color id
+};
+
+__device__ __forceinline__ bool stencil_cols(const Stencil& st, uint32_t i, int32_t (&c)[27]) {
+  const uint32_t col = i / st.n8;
+  uint32_t pos = i - col * st.n8;
+  const uint32_t Z = pos / st.hxy;
+  pos -= Z * st.hxy;
+  const uint32_t Y = pos / st.hx;
+  const uint32_t X = pos - Y * st.hx;
+  const int x = (int)(2 * X + ((col >> st.bx) & 1));
+  const int y = (int)(2 * Y + ((col >> st.by) & 1));
+  const int z = (int)(2 * Z + ((col >> st.bz) & 1));
+  if (x < 1 || x > st.lx - 2 || y < 1 || y > st.ly - 2 || z < 1 || z > st.lz - 2) return false;
+  int32_t px[3], py[3], pz[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int ax = x + d - 1, ay = y + d - 1, az = z + d - 1;
+    px[d] = (int32_t)((ax & 1 ? st.cx : 0u) + (uint32_t)(ax >> 1));
+    py[d] = (int32_t)((ay & 1 ? st.cy : 0u) + (uint32_t)(ay >> 1) * st.hx);
+    pz[d] = (int32_t)((az & 1 ? st.cz : 0u) + (uint32_t)(az >> 1) * st.hxy);
+  }
+#pragma unroll
+  for (int s = 0; s < 27; ++s) c[s] = pz[s / 9] + py[(s / 3) % 3] + px[s % 3];
+  c[13] = ~c[13];
+  return true;
+}
+
 // known0 >= 0: columns >= known0 are known to hold 0 (the smoother's zero
 // initial guess for colors not yet updated in this sweep, and the zeroed halo):
 // their products are still formed -- v * 0, the reference's arithmetic -- only
 // the load of a known zero is skipped.
 template <typename T, bool ZERO_DIAG, bool COHERENT = false, bool PDL = false>
 __device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, const T* __restrict__ vals,
-                                            int64_t ld, int64_t i, const T* x, T* d, int64_t known0 = -1) {
+                                            int64_t ld, int64_t i, const T* x, T* d, int64_t known0 = -1,
+                                            const Stencil st = Stencil{}) {
   int32_t c[27];
   T v[27];
   const uint64_t pol = stream_policy();
+  if (!(st.on && stencil_cols(st, (uint32_t)i, c))) {
 #pragma unroll
-  for (int s = 0; s < 27; ++s) c[s] = ld_stream(cols + s * ld + i, pol);
+    for (int s = 0; s < 27; ++s) c[s] = ld_stream(cols + s * ld + i, pol);
+  }
 #pragma unroll
   for (int s = 0; s < 27; ++s) v[s] = ld_stream(vals + s * ld + i, pol);
 #ifndef HPG_PIN_WAIT
@@ -185,7 +231,8 @@ __global__ void __launch_bounds__(256, 2) k_spmv(const int32_t* __restrict__ col
                                                  int64_t ld, int64_t row0, int64_t nrows,
                                                  const T* __restrict__ x, const T* __restrict__ b,
                                                  T* __restrict__ y, double* __restrict__ partial,
-                                                 const uint8_t* __restrict__ skip, const int32_t* __restrict__ list) {
+                                                 const uint8_t* __restrict__ skip, const int32_t* __restrict__ list,
+                                                 const Stencil st) {
   pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double sq = 0.0;
@@ -197,7 +244,7 @@ __global__ void __launch_bounds__(256, 2) k_spmv(const int32_t* __restrict__ col
   }
   if (active) {
     T dd;
-    const T acc = row_accumulate<T, false, false, MODE == 0>(cols, vals, ld, i, x, &dd);
+    const T acc = row_accumulate<T, false, false, MODE == 0>(cols, vals, ld, i, x, &dd, -1, st);
     if (MODE == 0) {
       y[i] = acc;
     } else {
@@ -225,9 +272,10 @@ __global__ void __launch_bounds__(256, 2) k_spmv(const int32_t* __restrict__ col
 //   z_i = (r_i - sum_{s != diag} A[i,s] z[col]) / a_ii
 template <typename T, bool COHERENT = false, bool PDL = false>
 __device__ __forceinline__ void gs_row(const int32_t* __restrict__ cols, const T* __restrict__ vals, int64_t ld,
-                                       int64_t i, const T* __restrict__ r, T* z, int64_t known0 = -1) {
+                                       int64_t i, const T* __restrict__ r, T* z, int64_t known0 = -1,
+                                       const Stencil st = Stencil{}) {
   T d = T(0);
-  const T acc = row_accumulate<T, true, COHERENT, PDL>(cols, vals, ld, i, z, &d, known0);
+  const T acc = row_accumulate<T, true, COHERENT, PDL>(cols, vals, ld, i, z, &d, known0, st);
   z[i] = div_rn(sub_rn(ldv<COHERENT>(r + i), acc), d);
 }
 
@@ -239,7 +287,8 @@ __global__ void __launch_bounds__(256, MINB) k_gs_pass(const int32_t* __restrict
                                                     int64_t ld, int64_t row0, int64_t nrows,
                                                     const T* __restrict__ r, T* z,
                                                     const uint8_t* __restrict__ skip,
-                                                    const int32_t* __restrict__ list, int64_t known0, int rev) {
+                                                    const int32_t* __restrict__ list, int64_t known0, int rev,
+                                                    const Stencil st) {
   pdl_trigger();
   // rev: blocks walk the color block from its end, so a pass starts on the
   // planes the previous pass finished last (their z lines are still in L2)
@@ -251,7 +300,7 @@ __global__ void __launch_bounds__(256, MINB) k_gs_pass(const int32_t* __restrict
     if (list) i = list[t];
     if (skip && skip[i]) return;
   }
-  gs_row<T, false, true>(cols, vals, ld, i, r, z, known0);
+  gs_row<T, false, true>(cols, vals, ld, i, r, z, known0, st);
 }
 
 // Fused residual + injection: for fine color-0 row j < nc,
@@ -259,9 +308,10 @@ __global__ void __launch_bounds__(256, MINB) k_gs_pass(const int32_t* __restrict
 template <typename T, bool COHERENT = false, bool PDL = false>
 __device__ __forceinline__ void restrict_row(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                              int64_t ld, int64_t j, const int32_t* __restrict__ dst,
-                                             const T* __restrict__ r, const T* z, T* __restrict__ rc) {
+                                             const T* __restrict__ r, const T* z, T* __restrict__ rc,
+                                             const Stencil st = Stencil{}) {
   T dd;
-  const T acc = row_accumulate<T, false, COHERENT, PDL>(cols, vals, ld, j, z, &dd);
+  const T acc = row_accumulate<T, false, COHERENT, PDL>(cols, vals, ld, j, z, &dd, -1, st);
   rc[dst[j]] = sub_rn(ldv<COHERENT>(r + j), acc);
 }
 
@@ -269,11 +319,11 @@ template <typename T>
 __global__ void __launch_bounds__(256, 2) k_restrict(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                                      int64_t ld, int64_t nc, const int32_t* __restrict__ dst,
                                                      const T* __restrict__ r, const T* __restrict__ z,
-                                                     T* __restrict__ rc) {
+                                                     T* __restrict__ rc, const Stencil st) {
   pdl_trigger();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nc) return;
-  restrict_row<T, false, true>(cols, vals, ld, j, dst, r, z, rc);
+  restrict_row<T, false, true>(cols, vals, ld, j, dst, r, z, rc, st);
 }
 
 // Injection transpose: z[j] += zc[dst[j]]  (ref: multigrid.py:131-137)
@@ -558,6 +608,19 @@ __global__ void k_build_inject(Geom gc, int32_t* __restrict__ dst) {
   const int y = (int)((j / gc.lx) % gc.ly);
   const int z = (int)(j / ((int64_t)gc.lx * gc.ly));
   dst[j] = (int32_t)iperm(gc, x, y, z);
+}
+
+// bad |= 1 when an implicit-index row's closed-form columns differ from its
+// stored ELL columns (the level then keeps streaming indices)
+__global__ void k_check_stencil(const int32_t* __restrict__ cols, int64_t ld, int64_t n, Stencil st,
+                                unsigned int* __restrict__ bad, unsigned long long* __restrict__ rows) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t c[27];
+  if (!stencil_cols(st, (uint32_t)i, c)) return;
+  atomicAdd(rows, 1ull);
+  for (int s = 0; s < 27; ++s)
+    if (c[s] != cols[s * ld + i]) atomicOr(bad, 1u);
 }
 
 // flag[i] = 1 when row i reads a halo slot (ref: problem.py:78-85 halo_row_split)

@@ -29,7 +29,8 @@ def main():
     n, ne = lv.A_hi.n_rows, lv.A_hi.n_cols_extended
     nnz = lv.A_hi.nnz_total
     out = {"local": a.local, "tail_rows": os.environ.get("HPG_TAIL_ROWS", "default"),
-           "zero_sweep_slots_per_row": ctx.level_info(0)["zero_sweep_slots"] / n}
+           "zero_sweep_slots_per_row": ctx.level_info(0)["zero_sweep_slots"] / n,
+           "stencil_rows_L0": ctx.level_info(0)["stencil_rows"] if os.environ.get("HPG_STENCIL", "1") != "0" else 0}
 
     def timeit(fn, reps=a.reps):
         fn()
@@ -140,7 +141,7 @@ def main():
     out["solve30_motif_s"] = tal.seconds
     if a.brief:
         keys = ("gs_sweep_L0_f32_us", "gs_sweep0_L0_f32_us", "zero_sweep_slots_per_row", "gs_sweep_L0_f64_us", "vcycle_f32_us", "vcycle_f64_us", "spmv_f32_us",
-                "cgs2_k30_us", "solve30_ms", "gs_sweep_L1_f32_us", "gs_sweep0_L1_f32_us", "gs_sweep_L2_f32_us",
+                "cgs2_k30_us", "solve30_ms", "spmv_f64_us", "residual_f64_us", "restrict_L0_f32_us", "stencil_rows_L0", "gs_sweep_L1_f32_us", "gs_sweep0_L1_f32_us", "gs_sweep_L2_f32_us",
                 "gs_sweep0_L2_f32_us", "gs_sweep_L3_f32_us", "gs_sweep0_L3_f32_us")
         print(a.brief, {k: round(v, 1) for k, v in out.items() if k in keys})
     else:
