@@ -157,6 +157,7 @@ struct Level {
   int32_t* iperm_d = nullptr;
   hpg::Stencil st{};           // implicit-index rows (st.on when the layout allows, checked at build)
   int64_t st_rows = 0;         // rows that skip their column-index loads
+  bool st_lower = false;       // the zero-guess sweep's lower ELL has implicit-index rows too
   hpg::WaveLevel wave;         // dataflow sweep plan (valid when wave_ok)
   bool wave_ok = false;
   int32_t* wave_items = nullptr;
@@ -461,7 +462,10 @@ int gs_lower_launch(hpg_ctx* c, Level& L, int col, const T* r, T* z) {
   const T* dg = sizeof(T) == 8 ? (const T*)L.dg64 : (const T*)L.dg32;
   const int rev = c->gs_rev && (col & 1);
   cudaError_t e =
-      launch_pdl(c, hpg::lower_kernel<T>(lc.w), grid_for(cnt), 256, lcols, lv, lc.ldc, a, cnt, dg, r, z, rev);
+      c->stencil && L.st.on && L.st_lower
+          ? launch_pdl(c, hpg::lower_st_kernel<T>(col), grid_for(cnt), 256, lcols, lv, lc.ldc, a, cnt, dg, r, z, rev,
+                       L.st)
+          : launch_pdl(c, hpg::lower_kernel<T>(lc.w), grid_for(cnt), 256, lcols, lv, lc.ldc, a, cnt, dg, r, z, rev);
   CUDA_TRY(e);
   ++c->launches;
   return HPG_OK;
@@ -1005,6 +1009,7 @@ int build_lower(hpg_ctx* c, Level& L) {
 int build_stencil(hpg_ctx* c, Level& L) {
   L.st = hpg::Stencil{};
   L.st_rows = 0;
+  L.st_lower = false;
   const Geom& g = L.g;
   if (!L.n || g.perm_tab || g.ncolors != 8 || ((g.lx | g.ly | g.lz) & 1) || g.lx < 2 || g.ly < 2 || g.lz < 2 ||
       L.n >= (int64_t{1} << 31))
@@ -1027,6 +1032,10 @@ int build_stencil(hpg_ctx* c, Level& L) {
   st.cx = st.n8 << st.bx;
   st.cy = st.n8 << st.by;
   st.cz = st.n8 << st.bz;
+  auto magic = [](uint64_t d) { return d == 1 ? uint64_t{0} : ~uint64_t{0} / d + 1; };  // ceil(2^64 / d); d = 1 special-cased
+  st.mn8 = magic(st.n8);
+  st.mhxy = magic(st.hxy);
+  st.mhx = magic(st.hx);
   void* scratch = nullptr;
   CUDA_TRY(cudaMalloc(&scratch, 16));
   CUDA_TRY(cudaMemsetAsync(scratch, 0, 16, c->stream));
@@ -1034,6 +1043,17 @@ int build_stencil(hpg_ctx* c, Level& L) {
   unsigned int* bad = (unsigned int*)((char*)scratch + 8);
   hpg::k_check_stencil<<<grid_for(L.n), 256, 0, c->stream>>>(L.cols, L.ld, L.n, st, bad, rows);
   LAUNCH_CHECK();
+  // lower ELL (zero-guess sweeps): the compile-time offset lists of
+  // k_gs_lower_st assume parity bits x->0, y->1, z->2 and W_c = lower_width(c)
+  bool lower = L.lower_ok && st.bx == 0 && st.by == 1 && st.bz == 2;
+  for (int k = 0; lower && k < 8; ++k) lower = L.lc[k].w == hpg::lower_width(k);
+  unsigned int* bad_lower = (unsigned int*)((char*)scratch + 12);
+  if (lower)
+    for (int k = 0; k < 8; ++k) {
+      hpg::check_lower_st_kernel(k)<<<grid_for(n8), 256, 0, c->stream>>>(L.lcols + L.lc[k].base, L.lc[k].ldc, n8, st,
+                                                                          bad_lower);
+      LAUNCH_CHECK();
+    }
   unsigned long long h[2] = {0, 0};
   CUDA_TRY(cudaMemcpyAsync(h, scratch, 16, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1041,6 +1061,7 @@ int build_stencil(hpg_ctx* c, Level& L) {
   if ((unsigned int)h[1] == 0) {
     L.st = st;
     L.st_rows = (int64_t)h[0];
+    L.st_lower = lower && (unsigned int)(h[1] >> 32) == 0;
   }
   return HPG_OK;
 }
@@ -1485,7 +1506,8 @@ int hpg_level_info(hpg_ctx* c, int l, int64_t* info, int ninfo) {
     ls += (L.lower_ok ? L.lc[k].w : hpg::kWidth) * (L.g.off[k + 1] - L.g.off[k]);
   tmp[17] = ls;
   tmp[18] = L.st.on ? L.st_rows : 0;  // rows on the implicit-index path
-  for (int k = 0; k < ninfo && k < 19; ++k) info[k] = tmp[k];
+  tmp[19] = L.st_lower ? 1 : 0;        // zero-guess sweeps on the implicit-index path
+  for (int k = 0; k < ninfo && k < 20; ++k) info[k] = tmp[k];
   return HPG_OK;
 }
 

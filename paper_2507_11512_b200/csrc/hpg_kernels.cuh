@@ -151,14 +151,23 @@ struct Stencil {
   uint32_t cx, cy, cz;       // color-block offset contributed by an odd x / y / z
   int lx, ly, lz;
   int bx, by, bz;            // parity bit of each axis in the color id
+  uint64_t mn8, mhxy, mhx;   // ceil(2^64 / d): q = umul64hi(i, m) == i / d exactly for i, d < 2^32
 };
 
+#ifndef HPG_ST_MAGIC
+#define HPG_ST_MAGIC 1
+#endif
+__device__ __forceinline__ uint32_t st_div(uint32_t a, uint32_t d, uint64_t m) {
+  if (HPG_ST_MAGIC) return d == 1 ? a : (uint32_t)__umul64hi((uint64_t)a, m);
+  return a / d;
+}
+
 __device__ __forceinline__ bool stencil_cols(const Stencil& st, uint32_t i, int32_t (&c)[27]) {
-  const uint32_t col = i / st.n8;
+  const uint32_t col = st_div(i, st.n8, st.mn8);
   uint32_t pos = i - col * st.n8;
-  const uint32_t Z = pos / st.hxy;
+  const uint32_t Z = st_div(pos, st.hxy, st.mhxy);
   pos -= Z * st.hxy;
-  const uint32_t Y = pos / st.hx;
+  const uint32_t Y = st_div(pos, st.hx, st.mhx);
   const uint32_t X = pos - Y * st.hx;
   const int x = (int)(2 * X + ((col >> st.bx) & 1));
   const int y = (int)(2 * Y + ((col >> st.by) & 1));
@@ -226,8 +235,11 @@ __device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, co
 // MODE 0: y = Ax.  MODE 1: y = b - Ax and per-block partial of sum y^2 (fp64 outer residual).
 // skip (nullable): rows with skip[i] != 0 are left alone (interior/boundary
 // split for the overlapped halo exchange); list (nullable): row t is list[t].
+#ifndef HPG_SPMV_MINB
+#define HPG_SPMV_MINB 2
+#endif
 template <typename T, int MODE, bool SPLIT = false>
-__global__ void __launch_bounds__(256, 2) k_spmv(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? HPG_SPMV_MINB : 2) k_spmv(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                                  int64_t ld, int64_t row0, int64_t nrows,
                                                  const T* __restrict__ x, const T* __restrict__ b,
                                                  T* __restrict__ y, double* __restrict__ partial,

@@ -144,6 +144,117 @@ __global__ void __launch_bounds__(256, lower_minb<T, W>()) k_gs_lower(const int3
   z[i] = div_rn(sub_rn(ri, acc), d);
 }
 
+// Implicit-index variant for the 8-color lattice (Stencil on, parity bits
+// x->0, y->1, z->2): for a color C the lower entries of an interior row are the
+// offsets whose neighbour color C ^ mask(d) is < C, in slot order -- a
+// compile-time list, so W = lower_width(C) and the columns of interior rows
+// follow from the row's coordinates like stencil_cols (checked at build).
+// Rows on a face of the box load their lower ELL columns.
+__host__ __device__ constexpr int lower_mask(int s) {
+  return ((s % 3) != 1 ? 1 : 0) | (((s / 3) % 3) != 1 ? 2 : 0) | ((s / 9) != 1 ? 4 : 0);
+}
+__host__ __device__ constexpr int lower_width(int C) {
+  int w = 0;
+  for (int s = 0; s < kWidth; ++s) w += s != kDiagSlot && (C ^ lower_mask(s)) < C;
+  return w;
+}
+__host__ __device__ constexpr int lower_dir(int C, int k) {
+  for (int s = 0; s < kWidth; ++s)
+    if (s != kDiagSlot && (C ^ lower_mask(s)) < C && k-- == 0) return s;
+  return -1;
+}
+
+template <int C, int W>
+__device__ __forceinline__ bool stencil_lower_cols(const Stencil& st, uint32_t j, int32_t (&c)[W]) {
+  const uint32_t Z = st_div(j, st.hxy, st.mhxy);
+  const uint32_t p = j - Z * st.hxy;
+  const uint32_t Y = st_div(p, st.hx, st.mhx);
+  const uint32_t X = p - Y * st.hx;
+  const int x = (int)(2 * X + (C & 1)), y = (int)(2 * Y + ((C >> 1) & 1)), z = (int)(2 * Z + (C >> 2));
+  if (x < 1 || x > st.lx - 2 || y < 1 || y > st.ly - 2 || z < 1 || z > st.lz - 2) return false;
+  int32_t px[3], py[3], pz[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int ax = x + d - 1, ay = y + d - 1, az = z + d - 1;
+    px[d] = (int32_t)((ax & 1 ? st.cx : 0u) + (uint32_t)(ax >> 1));
+    py[d] = (int32_t)((ay & 1 ? st.cy : 0u) + (uint32_t)(ay >> 1) * st.hx);
+    pz[d] = (int32_t)((az & 1 ? st.cz : 0u) + (uint32_t)(az >> 1) * st.hxy);
+  }
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const int s = lower_dir(C, k);
+    c[k] = pz[s / 9] + py[(s / 3) % 3] + px[s % 3];
+  }
+  return true;
+}
+
+template <typename T, int C>
+__global__ void __launch_bounds__(256, lower_minb<T, lower_width(C)>()) k_gs_lower_st(
+    const int32_t* __restrict__ lcols, const T* __restrict__ lvals, int64_t ldc, int64_t row0, int64_t nrows,
+    const T* __restrict__ dg, const T* __restrict__ r, T* z, int rev, const Stencil st) {
+  constexpr int W = lower_width(C);
+  pdl_trigger();
+  const int64_t blk = rev ? (int64_t)(gridDim.x - 1 - blockIdx.x) : (int64_t)blockIdx.x;
+  const int64_t j = blk * blockDim.x + threadIdx.x;
+  if (j >= nrows) return;
+  const int64_t i = row0 + j;
+  int32_t c[W > 0 ? W : 1];
+  T v[W > 0 ? W : 1];
+  const uint64_t pol = lower_hint<T>() ? evict_first_policy() : stream_policy();
+  if constexpr (W > 0) {
+    if (!stencil_lower_cols<C>(st, (uint32_t)j, c)) {
+#pragma unroll
+      for (int s = 0; s < W; ++s)
+        c[s] = lower_hint<T>() ? ld_stream_ef(lcols + s * ldc + j, pol) : ld_stream(lcols + s * ldc + j, pol);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < W; ++s) v[s] = lower_hint<T>() ? ld_stream_ef(lvals + s * ldc + j, pol) : ld_stream(lvals + s * ldc + j, pol);
+  const T d = dg[i];
+  if (W > 0) pdl_wait_after(v[0]);
+  else pdl_wait();
+  const T ri = r[i];
+  T g[W > 0 ? W : 1];
+#pragma unroll
+  for (int s = 0; s < W; ++s) g[s] = z[c[s]];
+  T acc = T(0);
+#pragma unroll
+  for (int s = 0; s < W; ++s) acc = add_rn(acc, mul_rn(v[s], g[s]));
+  z[i] = div_rn(sub_rn(ri, acc), d);
+}
+
+// bad |= 1 when an interior row's closed-form lower columns differ from the
+// stored lower ELL of color C (the level then keeps the index stream)
+template <int C>
+__global__ void k_check_lower_st(const int32_t* __restrict__ lcols, int64_t ldc, int64_t nrows, Stencil st,
+                                 unsigned int* __restrict__ bad) {
+  constexpr int W = lower_width(C);
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if constexpr (W > 0) {
+    if (j >= nrows) return;
+    int32_t c[W];
+    if (!stencil_lower_cols<C>(st, (uint32_t)j, c)) return;
+    for (int k = 0; k < W; ++k)
+      if (c[k] != lcols[k * ldc + j]) atomicOr(bad, 1u);
+  }
+}
+__host__ inline void (*check_lower_st_kernel(int color))(const int32_t*, int64_t, int64_t, Stencil, unsigned int*) {
+  void (*tab[])(const int32_t*, int64_t, int64_t, Stencil, unsigned int*) = {
+      k_check_lower_st<0>, k_check_lower_st<1>, k_check_lower_st<2>, k_check_lower_st<3>,
+      k_check_lower_st<4>, k_check_lower_st<5>, k_check_lower_st<6>, k_check_lower_st<7>};
+  return tab[color];
+}
+
+template <typename T>
+using LowerStKernel = void (*)(const int32_t*, const T*, int64_t, int64_t, int64_t, const T*, const T*, T*, int,
+                               const Stencil);
+template <typename T>
+__host__ LowerStKernel<T> lower_st_kernel(int color) {
+  LowerStKernel<T> tab[] = {k_gs_lower_st<T, 0>, k_gs_lower_st<T, 1>, k_gs_lower_st<T, 2>, k_gs_lower_st<T, 3>,
+                            k_gs_lower_st<T, 4>, k_gs_lower_st<T, 5>, k_gs_lower_st<T, 6>, k_gs_lower_st<T, 7>};
+  return tab[color];
+}
+
 template <typename T>
 using LowerKernel = void (*)(const int32_t*, const T*, int64_t, int64_t, int64_t, const T*, const T*, T*, int);
 

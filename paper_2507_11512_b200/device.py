@@ -10,7 +10,7 @@ from . import _lib
 from .comm import runtime
 
 INFO_KEYS = ("n", "n_ext", "nnz", "ncolors") + tuple(f"off{i}" for i in range(9)) + \
-    ("halo", "ld", "nneighbours", "device_bytes", "zero_sweep_slots", "stencil_rows")
+    ("halo", "ld", "nneighbours", "device_bytes", "zero_sweep_slots", "stencil_rows", "stencil_lower")
 
 
 class Context:
