@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -11,6 +12,9 @@ from .comm import runtime
 
 INFO_KEYS = ("n", "n_ext", "nnz", "ncolors") + tuple(f"off{i}" for i in range(9)) + \
     ("halo", "ld", "nneighbours", "device_bytes", "zero_sweep_slots", "stencil_rows", "stencil_lower")
+
+
+BOOL_DEFAULTS = {"stencil": 1, "lower": 1, "graphs": 1, "pdl": 1, "gs_rev": 1}
 
 
 class Context:
@@ -83,6 +87,15 @@ class Context:
 
     def set_option(self, key, value):
         self.call("hpg_set_option", key.encode(), int(value))
+        self.__dict__.setdefault("_opts", {})[key] = int(value)
+
+    def option(self, key):
+        """Current value of a boolean library option (set here, else HPG_<KEY>, else the default)."""
+        opts = self.__dict__.get("_opts", {})
+        if key in opts:
+            return opts[key]
+        env = os.environ.get("HPG_" + key.upper())
+        return BOOL_DEFAULTS[key] if env is None else int(env[:1] != "0")
 
     def sync(self):
         self.call("hpg_sync")

@@ -112,9 +112,22 @@ def count_vcycle(h, tally, dtype):
 
 
 def zero_sweep_bytes(h, w):
-    """Bytes one level-0 zero-initial-guess sweep streams (csrc/hpg_lower.cuh)."""
+    """Bytes one level-0 zero-initial-guess sweep streams (csrc/hpg_lower.cuh): lower
+    values, the column indices of the rows off the implicit-index path (pro rata), and
+    diagonal, r, z write plus the gathered z once."""
     info = h.ctx.level_info(0)
-    return info["zero_sweep_slots"] * (4 + w) + 4 * info["n"] * w
+    n, slots = info["n"], info["zero_sweep_slots"]
+    idx_rows = n - info["stencil_rows"] if info["stencil_lower"] and h.ctx.option("stencil") else n
+    return slots * w + 4 * slots * idx_rows // max(n, 1) + 4 * n * w
+
+
+def full_sweep_moved_bytes(h, w):
+    """Bytes one level-0 full sweep (8 color passes) streams: every value, the column
+    indices of the rows off the implicit-index path, r, z gathered once, z written."""
+    info = h.ctx.level_info(0)
+    n = info["n"]
+    idx_rows = n - info["stencil_rows"] if h.ctx.option("stencil") else n
+    return info["nnz"] * w + 27 * 4 * idx_rows + 3 * n * w
 
 
 def _inject_nnz(domain):

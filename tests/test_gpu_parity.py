@@ -359,6 +359,7 @@ def test_full_size_properties():
     from paper_2507_11512_b200.smoother import forward_gs_sweep
     h = _hier(256)
     ctx = h.ctx
+    assert ctx.level_info(0)["stencil_rows"] == 254 ** 3 and ctx.level_info(0)["stencil_lower"] == 1
     lv = h.levels[0]
     n, ne = lv.A_hi.n_rows, lv.A_hi.n_cols_extended
     b = generate_rhs(lv.A_hi).b
@@ -384,9 +385,61 @@ def test_full_size_properties():
         ctx.set_option("lower", 1)
         assert torch.equal(zs[0], zs[1])
         ref = h.apply(rr).clone()
-        for key, val in (("graphs", 0), ("gs_rev", 0), ("pdl", 0), ("wave", 0)):
+        for key, val in (("graphs", 0), ("gs_rev", 0), ("pdl", 0), ("wave", 0), ("stencil", 0)):
             ctx.set_option(key, val)
             assert torch.equal(h.apply(rr), ref), (key, dt)
-        for key, val in (("graphs", 1), ("gs_rev", 1), ("pdl", 1), ("wave", 1)):
+        for key, val in (("graphs", 1), ("gs_rev", 1), ("pdl", 1), ("wave", 1), ("stencil", 1)):
             ctx.set_option(key, val)
+    h.close()
+
+
+def test_implicit_index_rows():
+    """Interior rows compute their ELL columns in closed form (hpg_kernels.cuh
+    Stencil; the zero-guess lower sweep via per-color offset lists): the path is
+    taken by exactly the rows whose 27 neighbours are all local, and SpMV, the fp64
+    residual, full and zero-guess sweeps, restriction and the V-cycle give the same
+    bits with and without it."""
+    import ctypes as C
+    from paper_2507_11512_b200 import _lib
+    from paper_2507_11512_b200.krylov import spmv
+    from paper_2507_11512_b200.smoother import forward_gs_sweep
+    h = _hier(32)
+    ctx = h.ctx
+    for li, l in enumerate((32, 16, 8, 4)):
+        info = ctx.level_info(li)
+        assert info["stencil_rows"] == (l - 2) ** 3 and info["stencil_lower"] == 1, (li, info)
+    lv, lc = h.levels[0], h.levels[1]
+    n, ne = lv.A_hi.n_rows, lv.A_hi.n_cols_extended
+    gen = torch.Generator("cuda").manual_seed(11)
+    outs = {}
+    for st in (1, 0):
+        ctx.set_option("stencil", st)
+        res = []
+        for A, dt in ((lv.A_hi, torch.float64), (lv.A_lo, torch.float32)):
+            gen.manual_seed(11)
+            x = torch.randn(ne, dtype=dt, device="cuda", generator=gen)
+            r = torch.randn(n, dtype=dt, device="cuda", generator=gen)
+            res.append(spmv(A, x).cpu())
+            for zero in (True, False):
+                z = x.clone()
+                forward_gs_sweep(A, r, z, z_is_zero=zero)
+                res.append(z.cpu())
+            rc = torch.empty(lc.A_hi.n_rows, dtype=dt, device="cuda")
+            ctx.call("hpg_restrict", 0, _lib.F64 if dt == torch.float64 else _lib.F32, _lib.ptr(r), _lib.ptr(x),
+                     _lib.ptr(rc))
+            res.append(rc.cpu())
+            res.append(h.apply(r).cpu().clone())
+        b = torch.randn(n, dtype=torch.float64, device="cuda", generator=gen)
+        x = torch.randn(ne, dtype=torch.float64, device="cuda", generator=gen)
+        rr = torch.empty(n, dtype=torch.float64, device="cuda")
+        rho2 = C.c_double()
+        ctx.call("hpg_residual", _lib.ptr(b), _lib.ptr(x), _lib.ptr(rr), C.byref(rho2))
+        res += [rr.cpu(), rho2.value]
+        outs[st] = res
+    ctx.set_option("stencil", 1)
+    for a, b in zip(outs[1], outs[0]):
+        if isinstance(a, float):
+            assert a == b
+        else:
+            assert torch.equal(a, b)
     h.close()
