@@ -440,13 +440,13 @@ int gs_pass_launch(hpg_ctx* c, Level& L, int64_t a, int64_t cnt, const T* r, T* 
     CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3, true>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip,
                         list, known0, 0, stencil_of(c, L)));
   else if (c->gs_minb == 3)
-    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
+    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 3>, grid_for(cnt, HPG_GS_BLOCK), HPG_GS_BLOCK, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
                         known0, rev, stencil_of(c, L)));
   else if (c->gs_minb == 4)
-    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 4>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
+    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 4>, grid_for(cnt, HPG_GS_BLOCK), HPG_GS_BLOCK, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
                         known0, rev, stencil_of(c, L)));
   else
-    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 2>, grid_for(cnt), 256, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
+    CUDA_TRY(launch_pdl(c, hpg::k_gs_pass<T, 2>, grid_for(cnt, HPG_GS_BLOCK), HPG_GS_BLOCK, L.cols, vals, L.ld, a, cnt, r, z, skip, list,
                         known0, rev, stencil_of(c, L)));
   ++c->launches;
   return HPG_OK;
@@ -463,7 +463,8 @@ int gs_lower_launch(hpg_ctx* c, Level& L, int col, const T* r, T* z) {
   const int rev = c->gs_rev && (col & 1);
   cudaError_t e =
       c->stencil && L.st.on && L.st_lower
-          ? launch_pdl(c, hpg::lower_st_kernel<T>(col), grid_for(cnt), 256, lcols, lv, lc.ldc, a, cnt, dg, r, z, rev,
+          ? launch_pdl(c, hpg::lower_st_kernel<T>(col), grid_for(cnt, HPG_LOWER_BLOCK), HPG_LOWER_BLOCK, lcols, lv,
+                       lc.ldc, a, cnt, dg, r, z, rev,
                        L.st)
           : launch_pdl(c, hpg::lower_kernel<T>(lc.w), grid_for(cnt), 256, lcols, lv, lc.ldc, a, cnt, dg, r, z, rev);
   CUDA_TRY(e);
@@ -482,6 +483,8 @@ int gs_wave_launch(hpg_ctx* c, Level& L, const T* r, T* z, int zero) {
   const int32_t* cols = L.cols;
   const T* vals = vals_of<T>(L);
   int64_t ld = L.ld;
+  // (no implicit-index rows here: the extra kernel argument made the fp64 item
+  // loop spill, level-0 fp64 sweep 1028 -> 1223 us)
   void* args[] = {(void*)&cols, (void*)&vals, (void*)&ld, (void*)&r, (void*)&z, (void*)&L.wave, (void*)&zero};
   const void* fn = wave_fn<T>(c->wave_coh);
   CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(hpg::kWaveRows), args, 0,
@@ -1213,7 +1216,8 @@ int spmv_launch(hpg_ctx* c, Level& L, int64_t cnt, const T* x, T* y, const uint8
                         (const T*)vals_of<T>(L), L.ld, (int64_t)0, cnt, x, (const T*)nullptr, y, (double*)nullptr,
                         skip, list, stencil_of(c, L)));
   else
-    CUDA_TRY(launch_pdl(c, hpg::k_spmv<T, 0>, grid_for(cnt), 256, (const int32_t*)L.cols, (const T*)vals_of<T>(L),
+    CUDA_TRY(launch_pdl(c, hpg::k_spmv<T, 0>, grid_for(cnt, HPG_SPMV_BLOCK), HPG_SPMV_BLOCK, (const int32_t*)L.cols,
+                        (const T*)vals_of<T>(L),
                         L.ld, (int64_t)0, cnt, x, (const T*)nullptr, y, (double*)nullptr, skip, list,
                         stencil_of(c, L)));
   ++c->launches;

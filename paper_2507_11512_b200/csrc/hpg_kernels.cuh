@@ -238,8 +238,12 @@ __device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, co
 #ifndef HPG_SPMV_MINB
 #define HPG_SPMV_MINB 2
 #endif
+#ifndef HPG_SPMV_BLOCK
+#define HPG_SPMV_BLOCK 128  // measured fp32 SpMV: 128 454 us, 256 466
+#endif
 template <typename T, int MODE, bool SPLIT = false>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? HPG_SPMV_MINB : 2) k_spmv(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+__global__ void __launch_bounds__(MODE == 0 && !SPLIT ? HPG_SPMV_BLOCK : 256,
+                                  (sizeof(T) == 4 ? HPG_SPMV_MINB : 2) * 256 / (MODE == 0 && !SPLIT ? HPG_SPMV_BLOCK : 256)) k_spmv(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                                  int64_t ld, int64_t row0, int64_t nrows,
                                                  const T* __restrict__ x, const T* __restrict__ b,
                                                  T* __restrict__ y, double* __restrict__ partial,
@@ -294,8 +298,11 @@ __device__ __forceinline__ void gs_row(const int32_t* __restrict__ cols, const T
 // SPLIT: rows may be skipped (skip[i] != 0) or taken from a list (interior /
 // boundary halves of color 0 around an overlapped exchange); the plain
 // instantiation is the hot path and carries neither.
+#ifndef HPG_GS_BLOCK
+#define HPG_GS_BLOCK 64  // measured per level-0 fp32 sweep: 64 583 us, 128 591, 256 625, 512 800
+#endif
 template <typename T, int MINB = 2, bool SPLIT = false>
-__global__ void __launch_bounds__(256, MINB) k_gs_pass(const int32_t* __restrict__ cols, const T* __restrict__ vals,
+__global__ void __launch_bounds__(SPLIT ? 256 : HPG_GS_BLOCK, SPLIT ? MINB : MINB * 256 / HPG_GS_BLOCK) k_gs_pass(const int32_t* __restrict__ cols, const T* __restrict__ vals,
                                                     int64_t ld, int64_t row0, int64_t nrows,
                                                     const T* __restrict__ r, T* z,
                                                     const uint8_t* __restrict__ skip,

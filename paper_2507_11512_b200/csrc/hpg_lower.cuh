@@ -188,8 +188,11 @@ __device__ __forceinline__ bool stencil_lower_cols(const Stencil& st, uint32_t j
   return true;
 }
 
+#ifndef HPG_LOWER_BLOCK
+#define HPG_LOWER_BLOCK 256  // measured level-0 zero sweep: 256 260 us, 128 269
+#endif
 template <typename T, int C>
-__global__ void __launch_bounds__(256, lower_minb<T, lower_width(C)>()) k_gs_lower_st(
+__global__ void __launch_bounds__(HPG_LOWER_BLOCK, lower_minb<T, lower_width(C)>() * 256 / HPG_LOWER_BLOCK) k_gs_lower_st(
     const int32_t* __restrict__ lcols, const T* __restrict__ lvals, int64_t ldc, int64_t row0, int64_t nrows,
     const T* __restrict__ dg, const T* __restrict__ r, T* z, int rev, const Stencil st) {
   constexpr int W = lower_width(C);
