@@ -248,9 +248,15 @@ __global__ void __launch_bounds__(MODE == 0 && !SPLIT ? HPG_SPMV_BLOCK : 256,
                                                  const T* __restrict__ x, const T* __restrict__ b,
                                                  T* __restrict__ y, double* __restrict__ partial,
                                                  const uint8_t* __restrict__ skip, const int32_t* __restrict__ list,
-                                                 const Stencil st) {
+                                                 const Stencil st, int ilv) {
   pdl_trigger();
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // ilv > 1: consecutive CTAs take the same chunk position in ilv
+  // equal segments of the rows (the 8 color blocks), so the x lines a chunk
+  // gathers from every color block are reused in L2 by its co-resident
+  // siblings instead of being re-fetched once per color block
+  int64_t blk = blockIdx.x;
+  if (ilv > 1) blk = (int64_t)(blockIdx.x % ilv) * (gridDim.x / ilv) + blockIdx.x / ilv;
+  const int64_t t = blk * blockDim.x + threadIdx.x;
   double sq = 0.0;
   int64_t i = row0 + t;
   bool active = t < nrows;
@@ -279,7 +285,8 @@ __global__ void __launch_bounds__(MODE == 0 && !SPLIT ? HPG_SPMV_BLOCK : 256,
     if (threadIdx.x == 0) {
       double a = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += red[w];
-      partial[blockIdx.x] = a;
+      // indexed by the row chunk, so the fold order is independent of ilv
+      if (blk * blockDim.x < nrows) partial[blk] = a;
     }
   }
 }
