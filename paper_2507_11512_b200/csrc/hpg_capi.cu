@@ -1889,6 +1889,8 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   else if (!strcmp(key, "p2p")) c->p2p = value != 0 && !c->peer_sym.empty();
   else if (!strcmp(key, "overlap_rows")) c->overlap_rows = value;
   else if (!strcmp(key, "gs_minb")) c->gs_minb = (int)value;
+  else if (!strcmp(key, "spmv_ilv")) c->spmv_ilv[0] = (int)value;
+  else if (!strcmp(key, "spmv_ilv32")) c->spmv_ilv[1] = (int)value;
   else if (!strcmp(key, "wave")) c->wave = (int)value;
   else if (!strcmp(key, "wave_min_rows")) c->wave_min_rows = value;
   else if (!strcmp(key, "known_zero")) c->known_zero = value != 0;

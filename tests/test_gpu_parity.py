@@ -342,6 +342,41 @@ def test_execution_variants_agree_bitwise():
     h.close()
 
 
+@pytest.mark.parametrize("l", [24, 32])
+def test_spmv_interleave_bitwise(l):
+    """The SpMV CTA interleave over the color blocks (spmv_ilv / spmv_ilv32)
+    only reorders CTAs: y = A x and the fp64 residual r = b - A x with its
+    squared norm (block partials indexed by row chunk) are bitwise independent
+    of it, including grids that are not a multiple of the interleave (24^3)."""
+    import ctypes as C
+    from paper_2507_11512_b200 import _lib
+    h = _hier(l)
+    ctx, n = h.ctx, h.levels[0].A_hi.n_rows
+    g = torch.Generator("cuda").manual_seed(5)
+    x64 = torch.randn(n, device="cuda", dtype=torch.float64, generator=g)
+    b64 = torch.randn(n, device="cuda", dtype=torch.float64, generator=g)
+    x32 = x64.float()
+    outs = []
+    for ilv in (1, 3, 4, 8):
+        ctx.set_option("spmv_ilv", ilv)
+        ctx.set_option("spmv_ilv32", ilv)
+        y64 = torch.empty_like(x64)
+        y32 = torch.empty_like(x32)
+        r64 = torch.empty_like(x64)
+        ctx.call("hpg_spmv", 0, _lib.F64, _lib.ptr(x64), _lib.ptr(y64))
+        ctx.call("hpg_spmv", 0, _lib.F32, _lib.ptr(x32), _lib.ptr(y32))
+        rho2 = C.c_double()
+        ctx.call("hpg_residual", _lib.ptr(b64), _lib.ptr(x64), _lib.ptr(r64), C.byref(rho2))
+        torch.cuda.synchronize()
+        outs.append((y64.cpu().numpy(), y32.cpu().numpy(), r64.cpu().numpy(), rho2.value))
+    for o in outs[1:]:
+        for a, b in zip(o[:3], outs[0][:3]):
+            np.testing.assert_array_equal(a, b)
+        assert o[3] == outs[0][3]
+    np.testing.assert_array_equal(outs[0][2], b64.cpu().numpy() - outs[0][0])
+    h.close()
+
+
 def test_full_size_properties():
     """BASELINE configs[1] size (256^3 on one GPU), where the oracle is out of
     reach: size-independent identities, each exact.
