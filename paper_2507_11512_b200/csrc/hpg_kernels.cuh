@@ -236,7 +236,7 @@ __device__ __forceinline__ T row_accumulate(const int32_t* __restrict__ cols, co
 // skip (nullable): rows with skip[i] != 0 are left alone (interior/boundary
 // split for the overlapped halo exchange); list (nullable): row t is list[t].
 #ifndef HPG_SPMV_MINB
-#define HPG_SPMV_MINB 2
+#define HPG_SPMV_MINB 4  // fp32 (r01q/r01r A/B, 128-thread blocks): 2 (80 regs) 456 us, 4 (64 regs) 444, 5 (48 + spill) 450
 #endif
 #ifndef HPG_SPMV_BLOCK
 #define HPG_SPMV_BLOCK 128  // measured fp32 SpMV: 128 454 us, 256 466
