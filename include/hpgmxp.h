@@ -166,6 +166,9 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
  *   "known_zero" 1: zero-initial-guess sweeps skip the loads of not-yet-updated colors
  *   "gs_minb"    blocks per SM the color-pass kernel is compiled for (2 or 3)
  *   "gs_rev"     1: odd colors' passes walk their block backwards (L2 reuse at the turn)
+ *   "spmv_ilv"   fp64 SpMV / residual CTAs interleaved over this many row segments
+ *                (the color blocks) so x gathers hit L2 (default 4; bitwise identical)
+ *   "spmv_ilv32" the same for the fp32 SpMV (default 1)
  *   "wave"       bit mask (1 fp64, 2 fp32): forward sweeps as one dataflow kernel
  *                (bitwise identical; default 1) */
 int hpg_set_option(hpg_ctx* ctx, const char* key, int64_t value);
