@@ -109,8 +109,10 @@ class Box:
         return sorted(out)
 
 
-def make_boxes(lx, ly, lz, ranks):
-    px, py, pz = factor_ranks(ranks)
+def make_boxes(lx, ly, lz, ranks, dims=None):
+    """dims: an explicit (px, py, pz) process grid (default factor_ranks)."""
+    px, py, pz = factor_ranks(ranks) if dims is None else dims
+    assert px * py * pz == ranks
     return [Box(lx, ly, lz, r % px, (r // px) % py, r // (px * py), px, py, pz)
             for r in range(ranks)]
 
@@ -336,9 +338,9 @@ def injection_map(coarse, fine):
 class World:
     """All ranks of one problem; vectors are lists of per-rank arrays."""
 
-    def __init__(self, lx, ly, lz, ranks, levels):
+    def __init__(self, lx, ly, lz, ranks, levels, dims=None):
         self.ranks = ranks
-        boxes = make_boxes(lx, ly, lz, ranks)
+        boxes = make_boxes(lx, ly, lz, ranks, dims)
         self.levels = []           # levels[l][rank] -> RankLevel
         for lev in range(levels):
             per = [build_rank_level(b) for b in boxes]
@@ -506,8 +508,8 @@ def penalty_factor(n_d, n_ir):
 # ----------------------------------------------------------------------------
 
 class Solver:
-    def __init__(self, lx, ly, lz, ranks=1, levels=4, nu1=1, nu2=1, nu_c=1):
-        self.world = World(lx, ly, lz, ranks, levels)
+    def __init__(self, lx, ly, lz, ranks=1, levels=4, nu1=1, nu2=1, nu_c=1, dims=None):
+        self.world = World(lx, ly, lz, ranks, levels, dims)
         self.nlev = levels
         self.nu1, self.nu2, self.nu_c = nu1, nu2, nu_c
         self.count = Count()        # rank 0's tally (counts are per rank)
@@ -705,8 +707,8 @@ def back_substitute(H, t, k):
 # ----------------------------------------------------------------------------
 
 def run_validation(lx, ly, lz, ranks=1, levels=4, tol=1e-9, nd_cap=10000, m=30,
-                   mode="standard"):
-    s = Solver(lx, ly, lz, ranks, levels)
+                   mode="standard", dims=None):
+    s = Solver(lx, ly, lz, ranks, levels, dims=dims)
     b = s.rhs()
     dres, _ = s.gmres(b, "double", tol, nd_cap, m)
     if mode == "standard":

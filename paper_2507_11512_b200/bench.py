@@ -60,6 +60,9 @@ class BenchConfig:
     nu1: int = 1
     nu2: int = 1
     nu_c: int = 1
+    # (npx, npy, npz) for the job's ranks instead of factor_ranks(ranks) -- an
+    # extension of the reference, used to run x-axis splits on 2 and 4 GPUs
+    proc_grid: tuple = None
 
     def validate(self):
         if self.mg_levels < 1:
@@ -83,6 +86,9 @@ class BenchConfig:
              f"unknown validation mode {self.validation_mode!r}"),
             (self.coloring in COLORING_STRATEGIES, f"unknown coloring strategy {self.coloring!r}"),
             (min(self.nu1, self.nu2, self.nu_c) >= 1, "smoothing sweep counts must be at least 1"),
+            (self.proc_grid is None or (len(self.proc_grid) == 3 and min(self.proc_grid) >= 1 and
+                                        int(np.prod(self.proc_grid)) == self.ranks),
+             f"process grid {self.proc_grid} does not hold {self.ranks} ranks"),
         ]
         for ok, msg in checks:
             if not ok:
@@ -95,7 +101,8 @@ class BenchConfig:
 # -- per-rank state -------------------------------------------------------------
 
 def _build_state(cfg, nranks, world, rank):
-    gp = GlobalProblem.from_local(cfg.local_nx, cfg.local_ny, cfg.local_nz, nranks)
+    dims = cfg.proc_grid if (cfg.proc_grid is not None and nranks == cfg.ranks) else None
+    gp = GlobalProblem.from_local(cfg.local_nx, cfg.local_ny, cfg.local_nz, nranks, proc_dims=dims)
     hier = build_hierarchy(gp.domain(rank), cfg.mg_levels, world, rank,
                            strategy=cfg.coloring, seed=cfg.seed, sweeps=cfg.sweeps())
     lv = hier.levels[0]
@@ -139,16 +146,21 @@ def run_validation(cfg, world=None):
         nranks = cfg.validation_ranks
     else:
         nranks = cfg.ranks
-    if nranks not in (1, here.nranks):
-        raise ConfigError(f"validation on {nranks} of {here.nranks} ranks is not supported by the "
-                          "process-per-GPU world (use 1 or all ranks)")
+    if nranks > here.nranks:
+        raise ConfigError(f"validation on {nranks} ranks but the job has {here.nranks}")
     if nranks == 1:
         out = None
         if here.rank == 0:
             out = _validation_worker(None, 0, cfg, 1)
         out = here.broadcast_bytes(out)
-    else:
+    elif nranks == here.nranks:
         out = here.run(_validation_worker, cfg, nranks)[0]
+    else:
+        # the first `nranks` processes form the validation world (factor_ranks grid
+        # of nranks, ref: bench.py:165-167); the others wait for its result
+        sub = here.subworld(nranks)
+        out = sub.run(_validation_worker, cfg, nranks)[0] if sub is not None else None
+        out = here.broadcast_bytes(out)
     n_d, n_ir, res_d, _ = out
     return {"mode": cfg.validation_mode, "n_d": n_d, "n_ir": n_ir, "ratio": n_d / n_ir,
             "residual": res_d}

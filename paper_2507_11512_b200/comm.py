@@ -61,35 +61,58 @@ def runtime():
 
 
 class World:
-    """The set of ranks of one job (one process each); ``world=None`` means 1 rank."""
+    """The set of ranks of one job (one process each); ``world=None`` means 1 rank.
 
-    def __init__(self, nranks=None):
+    ``subworld(k)`` gives the first k ranks their own World (a gloo sub-group),
+    e.g. for a validation run on fewer ranks than the job (ref: bench.py:165-167).
+    """
+
+    def __init__(self, nranks=None, _group=None, _rank=None):
         import torch.distributed as dist
         if nranks is None:
             nranks = int(os.environ.get("WORLD_SIZE", "1"))
         if nranks < 1:
             raise ValueError(f"need at least one rank, got {nranks}")
         self.nranks = nranks
-        if nranks > 1 and not dist.is_initialized():
-            dist.init_process_group("gloo")
-        if nranks > 1 and dist.get_world_size() != nranks:
-            raise ProtocolError(f"world of {nranks} ranks requested but {dist.get_world_size()} "
-                                "processes are running (one process per rank)")
-        self.rank = dist.get_rank() if nranks > 1 else 0
+        self._group = _group
+        if _group is None:
+            if nranks > 1 and not dist.is_initialized():
+                dist.init_process_group("gloo")
+            if nranks > 1 and dist.get_world_size() != nranks:
+                raise ProtocolError(f"world of {nranks} ranks requested but {dist.get_world_size()} "
+                                    "processes are running (one process per rank)")
+            self.rank = dist.get_rank() if nranks > 1 else 0
+        else:
+            self.rank = _rank
         self._uid = None
+
+    def subworld(self, k):
+        """World of ranks [0, k) (collective over this world); None on the other ranks."""
+        if not 1 <= k <= self.nranks:
+            raise ValueError(f"sub-world of {k} ranks out of [1, {self.nranks}]")
+        if k == self.nranks:
+            return self
+        if k == 1:
+            return World(1) if self.rank == 0 else None
+        import torch.distributed as dist
+        g = dist.new_group(ranks=list(range(k)), backend="gloo")
+        return World(k, _group=g, _rank=self.rank) if self.rank < k else None
+
+    def _kw(self):
+        return {} if self._group is None else {"group": self._group}
 
     # -- control plane (host, gloo) -------------------------------------
     def barrier(self, rank=None):
         if self.nranks > 1:
             import torch.distributed as dist
-            dist.barrier()
+            dist.barrier(**self._kw())
 
     def broadcast_bytes(self, data, root=0):
         if self.nranks == 1:
             return data
         import torch.distributed as dist
         box = [data]
-        dist.broadcast_object_list(box, src=root)
+        dist.broadcast_object_list(box, src=root, **self._kw())  # members are ranks 0..k-1 globally
         return box[0]
 
     def gather(self, rank, value, root=0):
@@ -98,7 +121,7 @@ class World:
             return [value]
         import torch.distributed as dist
         out = [None] * self.nranks
-        dist.all_gather_object(out, value)
+        dist.all_gather_object(out, value, **self._kw())
         return out if rank == root else None
 
     def all_reduce_sum(self, rank, value):
@@ -107,7 +130,7 @@ class World:
             return value
         import torch.distributed as dist
         parts = [None] * self.nranks
-        dist.all_gather_object(parts, pickle.dumps(value))
+        dist.all_gather_object(parts, pickle.dumps(value), **self._kw())
         vals = [pickle.loads(p) for p in parts]
         acc = vals[0].copy() if isinstance(vals[0], np.ndarray) else vals[0]
         for v in vals[1:]:
@@ -132,7 +155,7 @@ class World:
             return [res]
         import torch.distributed as dist
         out = [None] * self.nranks
-        dist.all_gather_object(out, res)
+        dist.all_gather_object(out, res, **self._kw())
         return out
 
 

@@ -686,35 +686,37 @@ int vcycle(hpg_ctx* c, int l, const T* r, T* z) {
   return HPG_OK;
 }
 
+// Fixed-order fold of fp64 dot partials [cnt][nb] -> scal[0..cnt), the
+// rank-ordered all-reduce, then one rounding to T (+ sqrt for beta).
+template <typename T>
+int fold_dots(hpg_ctx* c, const double* part, int nb, int cnt, double* out, bool do_sqrt) {
+  hpg::k_fold<double><<<1, 1024, 0, c->stream>>>(part, nb, cnt, out, 0);
+  LAUNCH_CHECK();
+  ++c->launches;
+  int rc = allreduce_scal<double>(c, out, cnt);
+  if (rc) return rc;
+  hpg::k_round_dots<T><<<1, 64, 0, c->stream>>>(out, cnt, do_sqrt ? 1 : 0);
+  LAUNCH_CHECK();
+  ++c->launches;
+  return HPG_OK;
+}
+
 template <typename T, int KB>
 int cgs2_kb(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   const int64_t n = c->lev[0].n;
-  T* part = (T*)c->partial;
-  T* scal = (T*)c->scal;
+  double* part = (double*)c->partial;
+  double* scal = (double*)c->scal;
   const int nb = c->nb;
-  hpg::k_dots<T, KB><<<nb, 256, 0, c->stream>>>(Q, ldq, kb, w, n, part);
-  hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(part, nb, kb, scal, 0);
-  LAUNCH_CHECK();
-  c->launches += 2;
   int rc;
-  if ((rc = allreduce_scal<T>(c, scal, kb))) return rc;
+  hpg::k_dots<T, KB><<<nb, 256, 0, c->stream>>>(Q, ldq, kb, w, n, part);
+  if ((rc = fold_dots<T>(c, part, nb, kb, scal, false))) return rc;
   hpg::k_cgs_sub_dots<T, KB><<<nb, 256, 0, c->stream>>>(Q, ldq, kb, w, n, scal, part);
-  hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(part, nb, kb, scal + 64, 0);
-  LAUNCH_CHECK();
-  c->launches += 2;
-  if ((rc = allreduce_scal<T>(c, scal + 64, kb))) return rc;
+  if ((rc = fold_dots<T>(c, part, nb, kb, scal + 64, false))) return rc;
   hpg::k_cgs_sub_norm<T, KB><<<nb, 256, 0, c->stream>>>(Q, ldq, kb, w, n, scal + 64, part);
   LAUNCH_CHECK();
-  c->launches += 1;
+  c->launches += 3;
   if (qnext) {
-    hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(part, nb, 1, scal + 128, c->nranks == 1);
-    LAUNCH_CHECK();
-    c->launches += 1;
-    if (c->nranks > 1) {
-      if ((rc = allreduce_scal<T>(c, scal + 128, 1))) return rc;
-      hpg::k_sqrt_inplace<T><<<1, 1, 0, c->stream>>>(scal + 128);
-      c->launches += 1;
-    }
+    if ((rc = fold_dots<T>(c, part, nb, 1, scal + 128, true))) return rc;
     hpg::k_scale<T><<<grid_for(n), 256, 0, c->stream>>>(w, scal + 128, qnext, n);
     LAUNCH_CHECK();
     c->launches += 1;
@@ -729,8 +731,8 @@ int cgs2_fused(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   p.Q = Q;
   p.w = w;
   p.qnext = qnext;
-  p.partial = (T*)c->partial;
-  p.scal = (T*)c->scal;
+  p.partial = (double*)c->partial;
+  p.scal = (double*)c->scal;
   p.ldq = ldq;
   p.n = c->lev[0].n;
   p.kb = kb;
@@ -759,37 +761,28 @@ int cgs2_passes(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   p.Q = Q;
   p.w = w;
   p.qnext = qnext;
-  p.partial = (T*)c->partial;
-  p.scal = (T*)c->scal;
+  p.partial = (double*)c->partial;
+  p.scal = (double*)c->scal;
   p.ldq = ldq;
   p.n = c->lev[0].n;
   p.kb = kb;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   const int grid = 2 * sms;
-  T* scal = (T*)c->scal;
+  double* scal = (double*)c->scal;
   int rc;
-  hpg::k_cgs_onepass<T, WR, RPW, U, 0><<<grid, hpg::kCgsThreads, 0, c->stream>>>(p, (const T*)nullptr);
-  hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(p.partial, grid, kb, scal, 0);
+  hpg::k_cgs_onepass<T, WR, RPW, U, 0><<<grid, hpg::kCgsThreads, 0, c->stream>>>(p, (const double*)nullptr);
+  if ((rc = fold_dots<T>(c, p.partial, grid, kb, scal, false))) return rc;
+  hpg::k_cgs_onepass<T, WR, RPW, U, 1><<<grid, hpg::kCgsThreads, 0, c->stream>>>(p, (const double*)scal);
+  if ((rc = fold_dots<T>(c, p.partial, grid, kb, scal + 64, false))) return rc;
+  hpg::k_cgs_onepass<T, WR, RPW, U, 2><<<grid, hpg::kCgsThreads, 0, c->stream>>>(p, (const double*)(scal + 64));
   LAUNCH_CHECK();
-  c->launches += 2;
-  if ((rc = allreduce_scal<T>(c, scal, kb))) return rc;
-  hpg::k_cgs_onepass<T, WR, RPW, U, 1><<<grid, hpg::kCgsThreads, 0, c->stream>>>(p, (const T*)scal);
-  hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(p.partial, grid, kb, scal + 64, 0);
-  LAUNCH_CHECK();
-  c->launches += 2;
-  if ((rc = allreduce_scal<T>(c, scal + 64, kb))) return rc;
-  hpg::k_cgs_onepass<T, WR, RPW, U, 2><<<grid, hpg::kCgsThreads, 0, c->stream>>>(p, (const T*)(scal + 64));
-  LAUNCH_CHECK();
-  c->launches += 1;
+  c->launches += 3;
   if (qnext) {
-    hpg::k_fold<T><<<1, 1024, 0, c->stream>>>(p.partial, grid, 1, scal + 128, 0);
-    LAUNCH_CHECK();
-    if ((rc = allreduce_scal<T>(c, scal + 128, 1))) return rc;
-    hpg::k_sqrt_inplace<T><<<1, 1, 0, c->stream>>>(scal + 128);
+    if ((rc = fold_dots<T>(c, p.partial, grid, 1, scal + 128, true))) return rc;
     hpg::k_scale<T><<<grid_for(p.n), 256, 0, c->stream>>>(w, scal + 128, qnext, p.n);
     LAUNCH_CHECK();
-    c->launches += 3;
+    c->launches += 1;
   }
   return HPG_OK;
 }
@@ -875,7 +868,7 @@ int cgs2_launch_t(hpg_ctx* c, T* Q, int64_t ldq, int k, T* w, T* qnext) {
     }
     if (rc) return rc;
   }
-  CUDA_TRY(cudaMemcpyAsync(c->pinned, c->scal, 129 * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->pinned, c->scal, 129 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaEventRecord(c->ev_cgs, c->stream));
   c->cgs_pending_kb = kb;
   c->cgs_pending_es = (int)sizeof(T);
@@ -888,17 +881,12 @@ int cgs2_finish(hpg_ctx* c, double* out) {
   if (getenv("HPG_CGS_STREAMSYNC")) CUDA_TRY(cudaStreamSynchronize(c->stream));
   else CUDA_TRY(cudaEventSynchronize(c->ev_cgs));
   const int kb = c->cgs_pending_kb;
+  // fp64 slots holding values rounded to the solve's precision
   for (int j = 0; j < kb; ++j) {
-    if (c->cgs_pending_es == 8) {
-      out[j] = ((const double*)c->pinned)[j];
-      out[kb + j] = ((const double*)c->pinned)[64 + j];
-    } else {
-      out[j] = ((const float*)c->pinned)[j];
-      out[kb + j] = ((const float*)c->pinned)[64 + j];
-    }
+    out[j] = c->pinned[j];
+    out[kb + j] = c->pinned[64 + j];
   }
-  out[2 * kb] = !c->cgs_pending_norm ? 0.0
-                : c->cgs_pending_es == 8 ? ((const double*)c->pinned)[128] : ((const float*)c->pinned)[128];
+  out[2 * kb] = c->cgs_pending_norm ? c->pinned[128] : 0.0;
   c->cgs_pending_kb = 0;
   return HPG_OK;
 }
@@ -915,7 +903,7 @@ int gemv_launch(hpg_ctx* c, const T* Q, int64_t ldq, int k, T* out) {
   memset(&p, 0, sizeof p);
   p.Q = Q;
   p.w = out;
-  p.scal = (T*)c->scal + 320;
+  p.scal = (double*)c->scal + 320;
   p.ldq = ldq;
   p.n = c->lev[0].n;
   p.kb = k;
@@ -935,9 +923,9 @@ int gemv_t(hpg_ctx* c, const T* Q, int64_t ldq, int k, const double* y, T* out) 
   Timed tm(c, M_ORTHO);
   if (k > 64) return fail(HPG_E_UNSUPPORTED, "restart length %d exceeds 64", k);
   if (ldq % 32 || c->lev[0].n % (16 / (int)sizeof(T))) return fail(HPG_E_ARG, "unaligned basis for gemv");
-  T yt[64];
-  for (int j = 0; j < k; ++j) yt[j] = (T)y[j];
-  CUDA_TRY(cudaMemcpyAsync((T*)c->scal + 320, yt, k * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  double ys[64];
+  for (int j = 0; j < k; ++j) ys[j] = (double)(T)y[j];
+  CUDA_TRY(cudaMemcpyAsync((double*)c->scal + 320, ys, k * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   if (k <= 1) return gemv_launch<T, 1, 1, 8>(c, Q, ldq, k, out);
   if (k <= 2) return gemv_launch<T, 2, 1, 8>(c, Q, ldq, k, out);
   if (k <= 4) return gemv_launch<T, 4, 1, 8>(c, Q, ldq, k, out);
@@ -1881,6 +1869,15 @@ int hpg_p2p_open(hpg_ctx* c, const void* handles, int stride) {
   return HPG_OK;
 }
 
+// Captured V-cycle graphs bake in the kernel choice and launch arguments that
+// the options select, so every option change drops them (they are re-captured
+// on the next V-cycle).
+static void drop_graphs(hpg_ctx* c) {
+  if (!c->gcache.empty()) cudaStreamSynchronize(c->stream);
+  for (auto& e : c->gcache) cudaGraphExecDestroy(e.exec);
+  c->gcache.clear();
+}
+
 int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(HPG_E_ARG, "null argument");
   if (!strcmp(key, "cgs_fused")) c->cgs_fused = value != 0;
@@ -1895,20 +1892,13 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   else if (!strcmp(key, "wave_min_rows")) c->wave_min_rows = value;
   else if (!strcmp(key, "known_zero")) c->known_zero = value != 0;
   else if (!strcmp(key, "lower")) c->lower = value != 0;
-  else if (!strcmp(key, "graphs")) {
-    c->graphs = value != 0;
-    for (auto& e : c->gcache) cudaGraphExecDestroy(e.exec);
-    c->gcache.clear();
-  }
+  else if (!strcmp(key, "graphs")) c->graphs = value != 0;
   else if (!strcmp(key, "tail_rows")) c->tail_rows = value;
   else if (!strcmp(key, "tail_cluster")) set_tail_cluster(c, (int)value);
   else if (!strcmp(key, "gs_rev")) c->gs_rev = value != 0;
-  else if (!strcmp(key, "stencil")) {
-    c->stencil = value != 0;
-    for (auto& e : c->gcache) cudaGraphExecDestroy(e.exec);  // captured launches carry the old arguments
-    c->gcache.clear();
-  }
+  else if (!strcmp(key, "stencil")) c->stencil = value != 0;
   else return fail(HPG_E_ARG, "unknown option %s", key);
+  drop_graphs(c);
   return HPG_OK;
 }
 

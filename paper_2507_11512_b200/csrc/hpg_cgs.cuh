@@ -75,8 +75,8 @@ struct CgsParams {
   T* w;            // vector being orthogonalised (length >= round_up(n, 32))
                    // n must be a multiple of the 16-byte vector width (host checks)
   T* qnext;        // Q[k+1] (NULL: skip norm/normalise)
-  T* partial;      // [64][gridDim] per-CTA partials
-  T* scal;         // [0,64) h1, [64,128) h2, [128] beta
+  double* partial;  // [64][gridDim] per-CTA partials (fp64 accumulation)
+  double* scal;     // [0,64) h1, [64,128) h2, [128] beta -- values rounded to T
   int64_t ldq, n;
   int kb;
   P2PAr ar;        // multi-rank: NVLink all-reduce between passes (ar.nranks == 1: none)
@@ -89,26 +89,39 @@ struct CgsParams {
 constexpr int kCgsThreads = 256;
 constexpr int kCgsWarps = kCgsThreads / 32;
 
-// CTA 0 folds the per-CTA partials of cnt outputs into dst (fixed order); with
-// several ranks it then all-reduces dst over NVLink in ascending rank order
-// before the optional square root (ref: krylov.py:123, 268; comm.py:97-108).
+// Dot products accumulate in fp64 whatever T is: an fp32 x fp32 product is
+// exact in fp64, so every h / beta^2 is the exact dot up to fp64 rounding of the
+// sum, and is rounded to T once, after the cross-CTA and cross-rank folds.  The
+// result is (to within ~1e-16 relative) independent of the grid and of the rank
+// decomposition -- the reference's fp32 OpenBLAS dots are one of many fp32
+// orders, each landing within rounding noise of this value.
 template <typename T>
-__device__ __forceinline__ void cgs_fold(const T* partial, int cnt, T* dst, bool do_sqrt, const P2PAr& ar,
-                                         uint64_t seq) {
+__device__ __forceinline__ double round_dot(double a, bool do_sqrt) {
+  const T v = (T)a;
+  return (double)(do_sqrt ? sqrt(v) : v);  // beta = sqrt in T of the T-rounded w.w (ref: krylov.py:268)
+}
+
+// CTA 0 folds the per-CTA partials of cnt outputs into dst (fixed order); with
+// several ranks it then all-reduces dst over NVLink in ascending rank order,
+// then rounds to T (and takes the square root) (ref: krylov.py:123, 268;
+// comm.py:97-108).
+template <typename T>
+__device__ __forceinline__ void cgs_fold(const double* partial, int cnt, double* dst, bool do_sqrt,
+                                         const P2PAr& ar, uint64_t seq) {
   if (blockIdx.x != 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool multi = ar.nranks > 1;
   for (int j = warp; j < cnt; j += kCgsWarps) {
-    T a = T(0);
+    double a = 0.0;
     for (int b = lane; b < (int)gridDim.x; b += 32) a += __ldcg(partial + (int64_t)j * gridDim.x + b);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) dst[j] = (do_sqrt && !multi) ? sqrt(a) : a;
+    if (lane == 0) dst[j] = multi ? a : round_dot<T>(a, do_sqrt);
   }
   if (multi) {
     __syncthreads();
-    p2p_allreduce_block<T>(dst, cnt, ar, seq);
-    if (do_sqrt && threadIdx.x == 0) dst[0] = sqrt(dst[0]);
+    p2p_allreduce_block<double>(dst, cnt, ar, seq);
+    if (threadIdx.x < cnt) dst[threadIdx.x] = round_dot<T>(dst[threadIdx.x], do_sqrt);
   }
 }
 
@@ -132,7 +145,7 @@ struct CgsStream {
   int64_t t1;
   T hr[RPW];
 
-  __device__ __forceinline__ CgsStream(const CgsParams<T>& p_, const T* h, int64_t t1_) : p(p_), t1(t1_) {
+  __device__ __forceinline__ CgsStream(const CgsParams<T>& p_, const double* h, int64_t t1_) : p(p_), t1(t1_) {
     lane = threadIdx.x & 31;
     warp = threadIdx.x >> 5;
     rg = warp % WR;
@@ -141,7 +154,7 @@ struct CgsStream {
 #pragma unroll
     for (int r = 0; r < RPW; ++r) {
       const int j = rg + r * WR;
-      hr[r] = (MODE > 0 && j < kb) ? __ldcg(h + j) : T(0);
+      hr[r] = (MODE > 0 && j < kb) ? (T)__ldcg(h + j) : T(0);
     }
   }
 
@@ -178,7 +191,8 @@ struct CgsStream {
   }
 
   // consume one iteration (block-uniform: contains barriers when WR > 1)
-  __device__ __forceinline__ void process(int64_t tb, V (&q)[U][RPW], V (&wv)[U], T (&acc)[RPW], V* red) const {
+  __device__ __forceinline__ void process(int64_t tb, V (&q)[U][RPW], V (&wv)[U], double (&acc)[RPW],
+                                          V* red) const {
     if (MODE > 0) {
       if (WR > 1) {
         // this warp's share of the correction, then the sum over the row group (fixed order)
@@ -235,12 +249,13 @@ struct CgsStream {
 #pragma unroll
         for (int r = 0; r < RPW; ++r)
 #pragma unroll
-          for (int c = 0; c < VN; ++c) acc[r] = fma(vget<T>(q[u][r], c), vget<T>(wv[u], c), acc[r]);
+          for (int c = 0; c < VN; ++c)
+            acc[r] = fma((double)vget<T>(q[u][r], c), (double)vget<T>(wv[u], c), acc[r]);
     } else if (MODE == 2 && rg == 0) {
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int c = 0; c < VN; ++c) acc[0] = fma(vget<T>(wv[u], c), vget<T>(wv[u], c), acc[0]);
+        for (int c = 0; c < VN; ++c) acc[0] = fma((double)vget<T>(wv[u], c), (double)vget<T>(wv[u], c), acc[0]);
     }
   }
 };
@@ -250,7 +265,7 @@ struct CgsStream {
 // iteration i is consumed (two register sets, alternating); narrow bases use
 // one larger register set (U tiles) instead -- measured faster for kb <= 16.
 template <typename T, int WR, int RPW, int U, int MODE, bool PIPE>
-__device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const T* h, T (&acc)[RPW],
+__device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const double* h, double (&acc)[RPW],
                                          typename Vec16<T>::V* red) {
   using S = CgsStream<T, WR, RPW, U, MODE>;
   using V = typename S::V;
@@ -279,13 +294,13 @@ __device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const T* h, T (&
 }
 
 // rows -> partial[j][block]: lane reduce per warp, then element groups added in order
-template <typename T, int WR, int RPW>
-__device__ __forceinline__ void cgs_store_rows(const T (&acc)[RPW], int kb, T* partial, T* sacc) {
+template <int WR, int RPW>
+__device__ __forceinline__ void cgs_store_rows(const double (&acc)[RPW], int kb, double* partial, double* sacc) {
   constexpr int WE = kCgsWarps / WR;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int r = 0; r < RPW; ++r) {
-    T a = acc[r];
+    double a = acc[r];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if (lane == 0) sacc[warp * RPW + r] = a;
@@ -293,7 +308,7 @@ __device__ __forceinline__ void cgs_store_rows(const T (&acc)[RPW], int kb, T* p
   __syncthreads();
   if (threadIdx.x < kb) {
     const int j = threadIdx.x, rg = j % WR, r = j / WR;
-    T a = sacc[rg * RPW + r];
+    double a = sacc[rg * RPW + r];
     for (int e = 1; e < WE; ++e) a += sacc[(e * WR + rg) * RPW + r];
     partial[(int64_t)j * gridDim.x + blockIdx.x] = a;
   }
@@ -306,42 +321,42 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
   using V = typename Vec16<T>::V;
   cg::grid_group grid = cg::this_grid();
   __shared__ V red[WR > 1 ? U * kCgsWarps * 32 : 1];
-  __shared__ T sacc[kCgsWarps * RPW];
+  __shared__ double sacc[kCgsWarps * RPW];
   {  // pass A: h1
-    T acc[RPW];
+    double acc[RPW];
 #pragma unroll
-    for (int r = 0; r < RPW; ++r) acc[r] = T(0);
+    for (int r = 0; r < RPW; ++r) acc[r] = 0.0;
     cgs_pass<T, WR, RPW, U, 0, (RPW >= HPG_CGS_PIPE_MIN)>(p, nullptr, acc, red);
-    cgs_store_rows<T, WR, RPW>(acc, p.kb, p.partial, sacc);
+    cgs_store_rows<WR, RPW>(acc, p.kb, p.partial, sacc);
   }
   grid.sync();
-  cgs_fold(p.partial, p.kb, p.scal, false, p.ar, p.seq0);
+  cgs_fold<T>(p.partial, p.kb, p.scal, false, p.ar, p.seq0);
   grid.sync();
   {  // pass B: w -= Q^T h1 ; h2
-    T acc[RPW];
+    double acc[RPW];
 #pragma unroll
-    for (int r = 0; r < RPW; ++r) acc[r] = T(0);
+    for (int r = 0; r < RPW; ++r) acc[r] = 0.0;
     cgs_pass<T, WR, RPW, U, 1, (RPW >= HPG_CGS_PIPE_MIN)>(p, p.scal, acc, red);
-    cgs_store_rows<T, WR, RPW>(acc, p.kb, p.partial, sacc);
+    cgs_store_rows<WR, RPW>(acc, p.kb, p.partial, sacc);
   }
   grid.sync();
-  cgs_fold(p.partial, p.kb, p.scal + 64, false, p.ar, p.seq0 + 1);
+  cgs_fold<T>(p.partial, p.kb, p.scal + 64, false, p.ar, p.seq0 + 1);
   grid.sync();
   {  // pass C: w -= Q^T h2 ; beta^2 (row-group-0 warps hold the block's share)
-    T acc[RPW];
+    double acc[RPW];
 #pragma unroll
-    for (int r = 0; r < RPW; ++r) acc[r] = T(0);
+    for (int r = 0; r < RPW; ++r) acc[r] = 0.0;
     cgs_pass<T, WR, RPW, U, 2, (RPW >= HPG_CGS_PIPE_MIN)>(p, p.scal + 64, acc, red);
-    cgs_store_rows<T, WR, RPW>(acc, 1, p.partial, sacc);
+    cgs_store_rows<WR, RPW>(acc, 1, p.partial, sacc);
   }
   if (p.qnext == nullptr) return;
   grid.sync();
-  cgs_fold(p.partial, 1, p.scal + 128, true, p.ar, p.seq0 + 2);
+  cgs_fold<T>(p.partial, 1, p.scal + 128, true, p.ar, p.seq0 + 2);
   grid.sync();
   // pass D: Q[k+1] = w / beta  (ref: krylov.py:269-273), 16-byte vectors
   using VV = typename Vec16<T>::V;
   constexpr int VN = Vec16<T>::N;
-  const T bt = __ldcg(p.scal + 128);
+  const T bt = (T)__ldcg(p.scal + 128);
   const int64_t nv = p.n / VN;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
     const VV x = __ldcg((const VV*)p.w + v);
@@ -357,24 +372,24 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
 // passes).  MODE 0/1 write per-CTA row partials, MODE 2 the per-CTA norm share.
 template <typename T, int WR, int RPW, int U, int MODE>
 __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs_onepass(const __grid_constant__ CgsParams<T> p,
-                                                               const T* __restrict__ h) {
+                                                               const double* __restrict__ h) {
   using V = typename Vec16<T>::V;
   __shared__ V red[WR > 1 ? U * kCgsWarps * 32 : 1];
-  __shared__ T sacc[kCgsWarps * RPW];
-  T acc[RPW];
+  __shared__ double sacc[kCgsWarps * RPW];
+  double acc[RPW];
 #pragma unroll
-  for (int r = 0; r < RPW; ++r) acc[r] = T(0);
+  for (int r = 0; r < RPW; ++r) acc[r] = 0.0;
   cgs_pass<T, WR, RPW, U, MODE, (RPW >= HPG_CGS_PIPE_MIN)>(p, h, acc, red);
-  cgs_store_rows<T, WR, RPW>(acc, MODE == 2 ? 1 : p.kb, p.partial, sacc);
+  cgs_store_rows<WR, RPW>(acc, MODE == 2 ? 1 : p.kb, p.partial, sacc);
 }
 
 // out = Q[0:k]^T y (ref: krylov.py:288-289): one streaming pass over k rows,
-// same warp roles as CGS2; y (narrowed to T) sits in p.scal[0..k).
+// same warp roles as CGS2; y (narrowed to T, held as double) sits in p.scal[0..k).
 template <typename T, int WR, int RPW, int U>
 __global__ void __launch_bounds__(kCgsThreads, 2) k_gemv_combine(const __grid_constant__ CgsParams<T> p) {
   using V = typename Vec16<T>::V;
   __shared__ V red[WR > 1 ? U * kCgsWarps * 32 : 1];
-  T acc[RPW];
+  double acc[RPW];
   cgs_pass<T, WR, RPW, U, 3, (RPW >= HPG_CGS_PIPE_MIN)>(p, p.scal, acc, red);
 }
 

@@ -420,19 +420,20 @@ __device__ __forceinline__ void block_chunk(int64_t n, int64_t& lo, int64_t& hi)
 }
 
 // partial[j][b] = sum_{i in chunk b} Q[j][i] * w[i],  j < kb
+// (dot products accumulate in fp64 for every T; see hpg_cgs.cuh:round_dot)
 template <typename T, int KB>
 __global__ void __launch_bounds__(256) k_dots(const T* __restrict__ Q, int64_t ldq, int kb,
-                                              const T* __restrict__ w, int64_t n, T* __restrict__ partial) {
-  T acc[KB];
+                                              const T* __restrict__ w, int64_t n, double* __restrict__ partial) {
+  double acc[KB];
 #pragma unroll
-  for (int j = 0; j < KB; ++j) acc[j] = T(0);
+  for (int j = 0; j < KB; ++j) acc[j] = 0.0;
   int64_t lo, hi;
   block_chunk(n, lo, hi);
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const T wi = w[i];
 #pragma unroll
     for (int j = 0; j < KB; ++j)
-      if (j < kb) acc[j] = fma(Q[j * ldq + i], wi, acc[j]);
+      if (j < kb) acc[j] = fma((double)Q[j * ldq + i], (double)wi, acc[j]);
   }
   block_reduce_store<KB>(acc, kb, partial, gridDim.x);
 }
@@ -441,13 +442,14 @@ __global__ void __launch_bounds__(256) k_dots(const T* __restrict__ Q, int64_t l
 //   w_i -= sum_j Q[j][i] h[j];  partial[j][b] = sum Q[j][i] w_i(new)
 template <typename T, int KB>
 __global__ void __launch_bounds__(256) k_cgs_sub_dots(const T* __restrict__ Q, int64_t ldq, int kb,
-                                                      T* __restrict__ w, int64_t n, const T* __restrict__ h,
-                                                      T* __restrict__ partial) {
-  T acc[KB], hr[KB];
+                                                      T* __restrict__ w, int64_t n, const double* __restrict__ h,
+                                                      double* __restrict__ partial) {
+  double acc[KB];
+  T hr[KB];
 #pragma unroll
   for (int j = 0; j < KB; ++j) {
-    acc[j] = T(0);
-    hr[j] = j < kb ? h[j] : T(0);
+    acc[j] = 0.0;
+    hr[j] = j < kb ? (T)h[j] : T(0);
   }
   int64_t lo, hi;
   block_chunk(n, lo, hi);
@@ -463,7 +465,7 @@ __global__ void __launch_bounds__(256) k_cgs_sub_dots(const T* __restrict__ Q, i
     w[i] = wi;
 #pragma unroll
     for (int j = 0; j < KB; ++j)
-      if (j < kb) acc[j] = fma(q[j], wi, acc[j]);
+      if (j < kb) acc[j] = fma((double)q[j], (double)wi, acc[j]);
   }
   block_reduce_store<KB>(acc, kb, partial, gridDim.x);
 }
@@ -471,12 +473,12 @@ __global__ void __launch_bounds__(256) k_cgs_sub_dots(const T* __restrict__ Q, i
 // CGS pass-2 correction fused with the norm: w_i -= sum_j Q[j][i] h[j]; partial[b] = sum w_i^2
 template <typename T, int KB>
 __global__ void __launch_bounds__(256) k_cgs_sub_norm(const T* __restrict__ Q, int64_t ldq, int kb,
-                                                      T* __restrict__ w, int64_t n, const T* __restrict__ h,
-                                                      T* __restrict__ partial) {
+                                                      T* __restrict__ w, int64_t n, const double* __restrict__ h,
+                                                      double* __restrict__ partial) {
   T hr[KB];
 #pragma unroll
-  for (int j = 0; j < KB; ++j) hr[j] = j < kb ? h[j] : T(0);
-  T acc[1] = {T(0)};
+  for (int j = 0; j < KB; ++j) hr[j] = j < kb ? (T)h[j] : T(0);
+  double acc[1] = {0.0};
   int64_t lo, hi;
   block_chunk(n, lo, hi);
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
@@ -486,7 +488,7 @@ __global__ void __launch_bounds__(256) k_cgs_sub_norm(const T* __restrict__ Q, i
       if (j < kb) tsum = fma(Q[j * ldq + i], hr[j], tsum);
     const T wi = w[i] - tsum;
     w[i] = wi;
-    acc[0] = fma(wi, wi, acc[0]);
+    acc[0] = fma((double)wi, (double)wi, acc[0]);
   }
   block_reduce_store<1>(acc, 1, partial, gridDim.x);
 }
@@ -534,12 +536,22 @@ __global__ void k_sqrt_inplace(T* v) {
   v[0] = sqrt(v[0]);
 }
 
+// fp64-accumulated dots -> rounded to T (beta: square root in T of the rounded
+// w.w), held as double (ref: krylov.py:123, 268; hpg_cgs.cuh:round_dot)
+template <typename T>
+__global__ void k_round_dots(double* v, int cnt, int do_sqrt) {
+  const int j = threadIdx.x;
+  if (j >= cnt) return;
+  const T a = (T)v[j];
+  v[j] = (double)(do_sqrt ? sqrt(a) : a);
+}
+
 // Q[k+1] = w / beta  (0 when beta == 0)  (ref: krylov.py:267-273)
 template <typename T>
-__global__ void k_scale(const T* __restrict__ w, const T* __restrict__ beta, T* __restrict__ q, int64_t n) {
+__global__ void k_scale(const T* __restrict__ w, const double* __restrict__ beta, T* __restrict__ q, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const T bt = *beta;
+  const T bt = (T)*beta;
   q[i] = bt != T(0) ? div_rn(w[i], bt) : T(0);
 }
 

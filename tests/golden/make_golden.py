@@ -32,6 +32,19 @@ def _import_ref():
     return mxpbench
 
 
+def _problem(lx, ly, lz, ranks, dims=None):
+    """The reference's GlobalProblem; ``dims`` = an explicit (npx, npy, npz) grid
+    (the reference's frozen dataclass built directly -- its from_local always
+    factors, which never splits x below 8 ranks)."""
+    from mxpbench.geometry import GlobalProblem
+    if dims is None:
+        return GlobalProblem.from_local(lx, ly, lz, ranks)
+    px, py, pz = dims
+    assert px * py * pz == ranks
+    return GlobalProblem(nx=px * lx, ny=py * ly, nz=pz * lz, npx=px, npy=py, npz=pz,
+                         lnx=lx, lny=ly, lnz=lz)
+
+
 # ---------------------------------------------------------------------------
 # structure: ELL arrays, permutation, halo plans, injection maps
 # ---------------------------------------------------------------------------
@@ -55,6 +68,22 @@ STRUCT_CASES = {
     "r12": (4, 4, 2, 12, 1),
 }
 
+# explicit process grids that split x (x faces, xy / xz edges, corners below 8 ranks)
+XSPLIT_STRUCT = {
+    # name: (lx, ly, lz, ranks, levels, dims)
+    "x211": (4, 4, 4, 2, 2, (2, 1, 1)),
+    "x221": (4, 4, 4, 4, 2, (2, 2, 1)),
+    "x212": (4, 4, 4, 4, 2, (2, 1, 2)),
+    "x411": (4, 4, 4, 4, 1, (4, 1, 1)),
+}
+XSPLIT_KERNELS = {"kx211": (8, 2, 3, (2, 1, 1)), "kx221": (8, 4, 3, (2, 2, 1)), "kx212": (8, 4, 3, (2, 1, 2))}
+XSPLIT_SOLVES = [
+    # name, local, ranks, levels, m, max_iters, dims
+    ("x211l16", 16, 2, 4, 30, 300, (2, 1, 1)),
+    ("x221l8", 8, 4, 4, 30, 300, (2, 2, 1)),
+    ("x212l8", 8, 4, 4, 30, 300, (2, 1, 2)),
+]
+
 
 def _level_arrays(prefix, lv, out):
     A = lv.A_hi
@@ -76,15 +105,18 @@ def _level_arrays(prefix, lv, out):
         out[prefix + f"recv_{nb}"] = np.array([sl.start, sl.stop])
 
 
-def make_structure():
+def make_structure(xsplit=False):
     mx = _import_ref()
     from mxpbench.comm import RankWorld
     from mxpbench.geometry import GlobalProblem
     from mxpbench.multigrid import build_hierarchy
 
-    for name, (lx, ly, lz, ranks, levels) in STRUCT_CASES.items():
-        gp = GlobalProblem.from_local(lx, ly, lz, ranks)
+    cases = {k: v + (None,) for k, v in STRUCT_CASES.items()} if not xsplit else XSPLIT_STRUCT
+    for name, (lx, ly, lz, ranks, levels, dims) in cases.items():
+        gp = _problem(lx, ly, lz, ranks, dims)
         out = {"dims": np.array([lx, ly, lz, ranks, levels])}
+        if dims is not None:
+            out["proc_dims"] = np.array(dims)
 
         def worker(world, rank):
             return build_hierarchy(gp.domain(rank), levels, world, rank)
@@ -105,7 +137,7 @@ def make_structure():
 # kernels on random data (single rank 16^3, and 8 ranks of 4^3)
 # ---------------------------------------------------------------------------
 
-def make_kernels():
+def make_kernels(xsplit=False):
     _import_ref()
     from mxpbench.comm import RankWorld, exchange
     from mxpbench.geometry import GlobalProblem
@@ -146,14 +178,17 @@ def make_kernels():
             out[f"{tag}_vcycle"] = h.apply(r.copy()).copy()
         return out
 
-    for name, (l, ranks, levels) in {"k16": (16, 1, 4), "k8r8": (4, 8, 2),
-                                     "k8x8r8": (8, 8, 4), "k8r2": (8, 2, 3)}.items():
-        gp = GlobalProblem.from_local(l, l, l, ranks)
+    cases = {"k16": (16, 1, 4, None), "k8r8": (4, 8, 2, None), "k8x8r8": (8, 8, 4, None),
+             "k8r2": (8, 2, 3, None)} if not xsplit else XSPLIT_KERNELS
+    for name, (l, ranks, levels, dims) in cases.items():
+        gp = _problem(l, l, l, ranks, dims)
         if ranks == 1:
             parts = [run_rank(None, 0, gp, levels, 7)]
         else:
             parts = RankWorld(ranks).run(run_rank, gp, levels, 7)
         out = {"dims": np.array([l, l, l, ranks, levels])}
+        if dims is not None:
+            out["proc_dims"] = np.array(dims)
         for r, p in enumerate(parts):
             for k, v in p.items():
                 out[f"r{r}_{k}"] = v
@@ -182,8 +217,8 @@ def _solve_child(case):
     from mxpbench.geometry import GlobalProblem
     from mxpbench.multigrid import build_hierarchy
 
-    name, l, ranks, levels, m, max_iters = case
-    gp = GlobalProblem.from_local(l, l, l, ranks)
+    name, l, ranks, levels, m, max_iters = case[:6]
+    gp = _problem(l, l, l, ranks, case[6] if len(case) > 6 else None)
     result = {}
     orig = kry.givens_update
     for mode in ("double", "mixed"):
@@ -230,8 +265,9 @@ def _solve_child(case):
     return result
 
 
-def make_solves():
+def make_solves(xsplit=False):
     out = {}
+    cases = XSPLIT_SOLVES if xsplit else SOLVE_CASES
     for threads in ("1", "default"):
         env = dict(os.environ)
         env["PYTHONDONTWRITEBYTECODE"] = "1"
@@ -239,7 +275,7 @@ def make_solves():
             env["OPENBLAS_NUM_THREADS"] = "1"
         else:
             env.pop("OPENBLAS_NUM_THREADS", None)
-        for case in SOLVE_CASES:
+        for case in cases:
             cmd = [sys.executable, __file__, "--solve-child", json.dumps(case)]
             p = subprocess.run(cmd, env=env, capture_output=True, text=True, check=True)
             out.setdefault(case[0], {})[threads] = json.loads(p.stdout.strip().splitlines()[-1])
@@ -252,8 +288,9 @@ def make_solves():
                 path = r.pop("_xpath")
                 xs[f"{name}_{threads}_{mode}"] = np.load(path)
                 os.unlink(path)
-    np.savez_compressed(os.path.join(HERE, "solves_x.npz"), **xs)
-    with open(os.path.join(HERE, "solves.json"), "w") as f:
+    tag = "_xsplit" if xsplit else ""
+    np.savez_compressed(os.path.join(HERE, f"solves{tag}_x.npz"), **xs)
+    with open(os.path.join(HERE, f"solves{tag}.json"), "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)
 
 
@@ -335,6 +372,12 @@ if __name__ == "__main__":
         make_validation()
     if "jpl" in what:
         make_jpl()
+    if "xsplit" in what:  # explicit x-splitting process grids (written to separate files)
+        make_structure(xsplit=True)
+        make_kernels(xsplit=True)
+        make_solves(xsplit=True)
+    if "xsplit-kernels" in what:
+        make_kernels(xsplit=True)
 # MatrixMarket fixtures (tests/golden/mtx_sha256.json) were produced with:
 #   from mxpbench.bench import BenchConfig, dump_matrix
 #   dump_matrix(BenchConfig(local_nx=8, local_ny=8, local_nz=8), path)              -> "l8r1"

@@ -14,7 +14,13 @@ import hpgmxp_oracle as O
 from conftest import load_golden
 
 STRUCT = ["s468", "s16", "s8", "odd354", "odd7", "deg144", "deg414", "deg114", "deg111",
-          "r2", "r4", "r8", "r8x8", "r3", "r12"]
+          "r2", "r4", "r8", "r8x8", "r3", "r12",
+          # explicit process grids that split x (tests/golden/make_golden.py XSPLIT_STRUCT)
+          "x211", "x221", "x212", "x411"]
+
+
+def _dims(g):
+    return tuple(int(d) for d in g["proc_dims"]) if "proc_dims" in g else None
 
 
 def test_factor_ranks_matches_reference_table():
@@ -31,7 +37,7 @@ def test_factor_ranks_matches_reference_table():
 def test_structure_bitwise(case):
     g = load_golden(f"struct_{case}.npz")
     lx, ly, lz, ranks, levels = map(int, g["dims"])
-    w = O.World(lx, ly, lz, ranks, levels)
+    w = O.World(lx, ly, lz, ranks, levels, _dims(g))
     for r in range(ranks):
         for li in range(levels):
             p = f"r{r}_l{li}_"
@@ -52,11 +58,11 @@ def test_structure_bitwise(case):
                 assert [sl.start, sl.stop] == list(g[p + f"recv_{nb}"])
 
 
-@pytest.mark.parametrize("case", ["k16", "k8r8", "k8x8r8", "k8r2"])
+@pytest.mark.parametrize("case", ["k16", "k8r8", "k8x8r8", "k8r2", "kx211", "kx221", "kx212"])
 def test_kernels_bitwise(case):
     g = load_golden(f"kernels_{case}.npz")
     l, _, _, ranks, levels = map(int, g["dims"])
-    s = O.Solver(l, l, l, ranks, levels)
+    s = O.Solver(l, l, l, ranks, levels, dims=_dims(g))
     L0, L1 = s.L(0), s.L(1)
     for tag, dt in (("f64", np.float64), ("f32", np.float32)):
         xs = [g[f"r{q}_{tag}_x"] for q in range(ranks)]
@@ -172,3 +178,23 @@ def test_threaded_oracle_is_bitwise_identical():
     finally:
         O.set_threads(1)
     np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("case", ["x211l16", "x221l8", "x212l8"])
+def test_xsplit_solve_counts(case):
+    """x-splitting process grids: fp64 counts exact, mixed per cycle within the
+    reference envelope +-1 (tests/golden/solves_xsplit.json, from the reference)."""
+    gold = load_golden("solves_xsplit.json")[case]
+    l = int(case[5:])
+    dims = tuple(int(c) for c in case[1:4])
+    ranks = dims[0] * dims[1] * dims[2]
+    s = O.Solver(l, l, l, ranks, 4, dims=dims)
+    b = s.rhs()
+    d, _ = s.gmres(b, "double")
+    assert d["iterations"] == gold["1"]["double"]["iterations"]
+    mx, _ = s.gmres(b, "mixed")
+    refs = [gold[t]["mixed"]["cycle_iters"] for t in ("1", "default")]
+    assert all(len(r) == len(mx["cycle_iters"]) for r in refs)
+    for i, g in enumerate(mx["cycle_iters"]):
+        assert min(r[i] for r in refs) - 1 <= g <= max(r[i] for r in refs) + 1

@@ -47,21 +47,30 @@ def _worker(rank, world_size, port, q):
         uid = w.nccl_uid()
         allu = w.gather(rank, uid)
         out["uid"] = (len(uid) == 128 and len(set(allu)) == 1) if rank == 0 else len(uid) == 128
-        gp = GlobalProblem.from_local(4, 4, 4, world_size)
-        d = gp.domain(rank)
-        plan = HaloPlan.__new__(HaloPlan)
-        plan.domain = d
-        sends = {nb: len(v) for nb, v in plan.send_rows().items()}
-        _, cols, _, _, meta = host_level(d.local_dims, d.coords, d.proc_dims)
-        out["sends"] = sends
-        out["halo"] = meta["halo"]
-        out["n"] = meta["n"]
-        everyone = w.gather(rank, (sends, meta["halo"]))
-        if rank == 0:
-            # total sent to rank q by all peers == q's halo size
-            for q_ in range(world_size):
-                got = sum(everyone[r][0].get(q_, 0) for r in range(world_size))
-                out[f"mirror_{q_}"] = got == everyone[q_][1]
+        # validation sub-world of the first k ranks (ref: bench.py:165-167)
+        k = world_size - 1
+        sub = w.subworld(k)
+        if rank < k:
+            out["subworld"] = (sub.nranks == k and sub.all_reduce_sum(rank, rank + 1) == k * (k + 1) // 2
+                               and sub.run(lambda world, r: r) == list(range(k)))
+        else:
+            out["subworld"] = sub is None
+        w.barrier()
+        # default factor_ranks grid, and x-axis splits through the process-grid override
+        grids = [None, (world_size, 1, 1)] + ([(2, 2, 1), (2, 1, 2)] if world_size == 4 else [])
+        for gi, dims in enumerate(grids):
+            gp = GlobalProblem.from_local(4, 4, 4, world_size, proc_dims=dims)
+            d = gp.domain(rank)
+            plan = HaloPlan.__new__(HaloPlan)
+            plan.domain = d
+            sends = {nb: len(v) for nb, v in plan.send_rows().items()}
+            _, cols, _, _, meta = host_level(d.local_dims, d.coords, d.proc_dims)
+            everyone = w.gather(rank, (sends, meta["halo"]))
+            if rank == 0:
+                # total sent to rank q by all peers == q's halo size
+                for q_ in range(world_size):
+                    got = sum(everyone[r][0].get(q_, 0) for r in range(world_size))
+                    out[f"mirror_{gi}_{q_}"] = got == everyone[q_][1] and got > 0
     except Exception as e:  # report, do not hang the parent
         out["error"] = repr(e)
     q.put((rank, out))
@@ -81,6 +90,7 @@ def test_world_over_gloo(world_size):
     for r, out in res.items():
         assert "error" not in out, out
         assert out["allreduce_ordered"] and out["gather"] and out["runs"] and out["uid"], out
+        assert out["subworld"], out
     for k, v in res[0].items():
         if k.startswith("mirror_"):
             assert v, (k, res)

@@ -18,6 +18,8 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 def main():
     L = int(sys.argv[1]) if len(sys.argv) > 1 else 8
     levels = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    # optional explicit process grid "px,py,pz" (x-axis splits on 2 / 4 GPUs)
+    dims = tuple(int(v) for v in sys.argv[3].split(",")) if len(sys.argv) > 3 else None
     import torch
     import hpgmxp_oracle as O
     from paper_2507_11512_b200.comm import World
@@ -29,12 +31,12 @@ def main():
 
     world = World()
     rank, R = world.rank, world.nranks
-    gp = GlobalProblem.from_local(L, L, L, R)
+    gp = GlobalProblem.from_local(L, L, L, R, proc_dims=dims)
     h = build_hierarchy(gp.domain(rank), levels, world, rank)
     lv = h.levels[0]
     A, Alo = lv.A_hi, lv.A_lo
     n, ne = A.n_rows, A.n_cols_extended
-    ora = O.Solver(L, L, L, R, levels)
+    ora = O.Solver(L, L, L, R, levels, dims=dims)
     ok = {}
     # structure
     OL = ora.L(0)[rank]
@@ -76,10 +78,11 @@ def main():
     # ranks) + timed phases; builds two more hierarchies (fresh NCCL communicators)
     from paper_2507_11512_b200.bench import BenchConfig, run_benchmark
     rep = run_benchmark(BenchConfig(local_nx=L, local_ny=L, local_nz=L, ranks=R, time_seconds=0,
-                                    mg_levels=levels, validation_mode="fullscale"))
+                                    mg_levels=levels, validation_mode="fullscale", proc_grid=dims))
     allok = world.gather(rank, ok)
     if rank == 0:
-        print(json.dumps({"ranks": R, "local": L, "checks": allok, "solves": res,
+        print(json.dumps({"ranks": R, "local": L, "proc_dims": list(gp.domain(0).proc_dims),
+                          "checks": allok, "solves": res,
                           "validation": rep["validation"], "summary": rep["summary"]}))
 
 
