@@ -28,6 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "HPG-MxP GFLOP/s (mixed, and speedup vs fp64) at 1/2/4/8 B200; % HBM roofline"
+GS_KERNEL = "k_gs_pass<float> level-0 color pass (multicolor GS, fp32; full and zero-guess sweeps)"
 UNIT = "GFLOP/s"
 
 
@@ -205,33 +206,57 @@ def run_ours(args):
     # warm-up
     for _ in range(args.warmup):
         _solve(cfg, hier, lv, b, world, rank, "mixed", cfg.tol, cfg.max_iters)
-    # flops of one solve (model, this rank) -- count on a tallied solve
-    tal = Tally()
-    res = _solve(cfg, hier, lv, b, world, rank, "mixed", cfg.tol, cfg.max_iters, tal)
-    flops_rank = tal.total_flops()
-    bytes_rank = tal.total_bytes()
-    gs_bytes = tal.bytes["GS"]
-    gs_sec = tal.seconds["GS"]
+
+    def tallied(mode):
+        """One tallied solve: model flops/bytes, executed flops, moved bytes (this rank)."""
+        t = Tally()
+        r = _solve(cfg, hier, lv, b, world, rank, mode, cfg.tol, cfg.max_iters, t)
+        return t, r
+
+    # flops of one solve (model, this rank) -- counted on a tallied solve; every
+    # timed solve must take the same path (same iteration count)
+    tal, res = tallied("mixed")
+    flops_rank, xflops_rank = tal.total_flops(), tal.total_exec_flops()
+    bytes_rank, moved_rank = tal.total_bytes(), tal.total_moved_bytes()
 
     clocks = Clocks(rt.device.index)
     clocks.start()
     dev_s, wall_s, iters, launches, last = timed("mixed", args.steps)
     clk = clocks.stop()
+    if any(it != res.iterations for it in iters):
+        raise RuntimeError(f"timed solves took {iters} iterations, the tallied one {res.iterations}")
     # timing of the dominant motif (GS) inside a timed solve: library CUDA events
-    tal2 = Tally()
-    _solve(cfg, hier, lv, b, world, rank, "mixed", cfg.tol, cfg.max_iters, tal2)
+    tal2, _ = tallied("mixed")
     gs_bytes, gs_sec = tal2.bytes["GS"], tal2.seconds["GS"]
     l0_bytes, l0_sec, l0_sweeps = tal2.gs_level0_bytes, tal2.gs_level0_seconds, tal2.gs_level0_sweeps
-    l0z_bytes, l0z_sec, l0z_sweeps = tal2.gs_level0z_bytes, tal2.gs_level0z_seconds, tal2.gs_level0z_sweeps
     ncolors = ctx.level_info(0)["ncolors"]
     from paper_2507_11512_b200.multigrid import full_sweep_moved_bytes
     l0_moved = full_sweep_moved_bytes(hier, 4) * l0_sweeps
 
     # fp64 comparison (same solves in double)
-    dtal = Tally()
-    _solve(cfg, hier, lv, b, world, rank, "double", cfg.tol, cfg.max_iters, dtal)
+    dtal, dres = tallied("double")
     dflops_rank = dtal.total_flops()
     ddev_s, dwall_s, diters, _, _ = timed("double", args.steps)
+    if any(it != dres.iterations for it in diters):
+        raise RuntimeError(f"timed fp64 solves took {diters} iterations, the tallied one {dres.iterations}")
+
+    # labelled variants of the mixed solve (same problem, same iteration counts):
+    #   general_ell: every row loads its column indices (no implicit-index rows)
+    #   lower_sweep: zero-initial-guess sweeps form only the strictly-lower products
+    #                (bitwise-identical results, fewer executed flops than counted)
+    variants = {}
+    for name, opts in (("general_ell", {"stencil": 0}), ("lower_sweep", {"lower": 1})):
+        for k, v in opts.items():
+            ctx.set_option(k, v)
+        _solve(cfg, hier, lv, b, world, rank, "mixed", cfg.tol, cfg.max_iters)  # re-capture graphs
+        vt, vr = tallied("mixed")
+        vdev, _, viters, _, _ = timed("mixed", args.steps)
+        if any(it != vr.iterations for it in viters):
+            raise RuntimeError(f"{name}: timed solves took {viters} iterations, the tallied one {vr.iterations}")
+        variants[name] = [vdev, vt.total_flops(), vt.total_exec_flops(), vt.total_bytes(), vt.total_moved_bytes()]
+        for k in opts:
+            ctx.set_option(k, {"stencil": 1, "lower": 0}[k])
+    _solve(cfg, hier, lv, b, world, rank, "mixed", cfg.tol, cfg.max_iters)
 
     # e2e through the public API with host buffers (H2D b, D2H x inside the region)
     # pinned host buffers (the public API accepts numpy arrays; pinned ones DMA directly)
@@ -258,7 +283,13 @@ def run_ours(args):
         return [op(p[i] for p in parts) for i in range(len(vals))]
 
     dev_s, ddev_s, e2e_s, wall_s = reduce([dev_s, ddev_s, e2e_s, wall_s], max)
-    flops_all, dflops_all, bytes_all = reduce([flops_rank, dflops_rank, bytes_rank], sum)
+    flops_all, xflops_all, dflops_all, bytes_all, moved_all = reduce(
+        [flops_rank, xflops_rank, dflops_rank, bytes_rank, moved_rank], sum)
+    vsum = {}
+    for name, (vdev, vf, vx, vb, vm) in variants.items():
+        vdev = reduce([vdev], max)[0]
+        vf, vx, vb, vm = reduce([vf, vx, vb, vm], sum)
+        vsum[name] = (vdev, vf, vx, vb, vm)
     hier.close()
     if rank != 0:
         return 0
@@ -270,17 +301,25 @@ def run_ours(args):
     fp64 = dflops_all * K / ddev_s / 1e9
     gs_gbs = gs_bytes / gs_sec / 1e9 if gs_sec > 0 else 0.0
     l0_gbs = l0_bytes / l0_sec / 1e9 if l0_sec > 0 else 0.0
-    l0z_gbs = l0z_bytes / l0z_sec / 1e9 if l0z_sec > 0 else 0.0
     l0_launches = l0_sweeps * ncolors
-    traffic = None
+    traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tr = json.load(f)
-        if tr.get("local") == L:
-            traffic = tr["gs_pass_level0_f32_dram_bytes_per_launch"]
+        if tr.get("local") == L and tr.get("kernel") == GS_KERNEL:
+            traffic, traffic_src = tr["gs_pass_level0_f32_dram_bytes_per_launch"], tr["source"]
     except (OSError, KeyError, ValueError):
         pass
     cpu_g, cpu_s = cpu_port_sample() if nproc == 1 and not args.no_cpu else (None, None)
+    pk = peak * nproc
+
+    def vline(vdev, vf, vx, vb, vm):
+        g = vf * K / vdev / 1e9
+        return {"gflops": g * (penalty if penalty is not None else 1.0), "raw_gflops": g,
+                "executed_gflops": vx * K / vdev / 1e9, "ms_per_solve": 1e3 * vdev / K,
+                "model_bytes_per_solve": vb, "moved_bytes_per_solve": vm,
+                "frac_model": vb * K / vdev / 1e9 / pk, "frac_moved": vm * K / vdev / 1e9 / pk}
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": nproc, "steps": K,
         "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / K, "higher_is_better": True,
@@ -288,19 +327,35 @@ def run_ours(args):
         "data": "synthetic (the benchmark's own generated 27-point problem, b = A*1)",
         "config": _config(L, nproc),
         "raw_gflops": raw, "penalty": penalty,
+        "executed_gflops": xflops_all * K / dev_s / 1e9,
+        "flops_note": "value counts the reference's frozen flop model (metrics.py:7-16); the "
+                      "headline kernels form every counted product (zero-guess sweeps included, "
+                      "as the reference does), so executed_gflops == raw_gflops",
         "validation": val, "iterations_per_solve": iters,
         "fp64_gflops": fp64, "fp64_iterations_per_solve": diters,
         "speedup_vs_fp64": value / fp64 if fp64 else None,
-        "solve_roofline": {"model_bytes_per_solve": bytes_all,
+        "solve_roofline": {"model_bytes_per_solve": bytes_all, "moved_bytes_per_solve": moved_all,
                            "achieved_gbs": bytes_all * K / dev_s / 1e9,
-                           "peak_gbs": peak * nproc,
-                           "frac": bytes_all * K / dev_s / 1e9 / (peak * nproc),
-                           "note": "reference byte model (metrics.py:37-77); the zero-initial-guess "
-                                   "sweeps stream only the strictly-lower part, fewer bytes than modelled"},
+                           "achieved_moved_gbs": moved_all * K / dev_s / 1e9,
+                           "peak_gbs": pk,
+                           "frac": bytes_all * K / dev_s / 1e9 / pk,
+                           "frac_moved": moved_all * K / dev_s / 1e9 / pk,
+                           "note": "frac: reference byte model (metrics.py:37-77), model-equivalent -- "
+                                   "implicit-index rows do not load the 4-B column index it charges; "
+                                   "frac_moved: the bytes the kernels move (model minus those indices)"},
+        "variants": {
+            "general_ell": dict(vline(*vsum["general_ell"]),
+                                note="stencil=0: every row loads its int32 column index plane (the "
+                                     "paper's general ELL; model bytes == moved bytes)"),
+            "lower_sweep": dict(vline(*vsum["lower_sweep"]),
+                                note="lower=1: zero-initial-guess sweeps form only the strictly-lower "
+                                     "products (bitwise-identical z); gflops counts the model, "
+                                     "executed_gflops what ran"),
+        },
         "roofline": {"bound": "hbm",
-                     "kernel": "k_gs_pass<float> level-0 color pass (multicolor GS, fp32, full sweeps)",
+                     "kernel": GS_KERNEL,
                      "achieved": l0_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": l0_gbs / peak, "traffic": traffic,
+                     "frac": l0_gbs / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": (l0_bytes / l0_launches) if l0_launches else None,
                      "avg_launch_us": (l0_sec / l0_launches * 1e6) if l0_launches else None,
                      "model_equivalent": True,
@@ -313,12 +368,6 @@ def run_ours(args):
                      "timing": "library CUDA events around every level-0 sweep of one timed solve",
                      "peak_kind": peak_kind,
                      "gs_all_levels_gbs": gs_gbs},
-        "zero_sweep_roofline": {
-            "kernel": "k_gs_lower_st<float,C> level-0 zero-initial-guess sweep (strictly-lower part, "
-                      "implicit-index interior rows; bitwise equal to the full sweep)",
-            "achieved": l0z_gbs, "peak": peak, "unit": "GB/s", "frac": l0z_gbs / peak,
-            "bytes_per_sweep": (l0z_bytes / l0z_sweeps) if l0z_sweeps else None,
-            "avg_sweep_us": (l0z_sec / l0z_sweeps * 1e6) if l0z_sweeps else None},
         "e2e": {"value": value * dev_s / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * 8,
                 "d2h_bytes_per_step": n * 8},
         "gpu_launches": launches,

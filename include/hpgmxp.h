@@ -170,7 +170,14 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
  *                (the color blocks) so x gathers hit L2 (default 4; bitwise identical)
  *   "spmv_ilv32" the same for the fp32 SpMV (default 1)
  *   "wave"       bit mask (1 fp64, 2 fp32): forward sweeps as one dataflow kernel
- *                (bitwise identical; default 1) */
+ *                (bitwise identical; default 1)
+ *   "wave_min_rows" levels with fewer rows keep the per-color passes
+ *   "lower"      1: zero-initial-guess sweeps run the strictly-lower kernel (bitwise
+ *                identical, but it skips the products against z = 0 that the
+ *                reference forms and the flop model counts; default 0)
+ *   "stencil"    1: rows whose 27 neighbours are local compute their columns in
+ *                closed form instead of loading the index plane (default 1)
+ * Every option change drops the captured V-cycle graphs (re-captured on next use). */
 int hpg_set_option(hpg_ctx* ctx, const char* key, int64_t value);
 
 /* NVLink peer memory (csrc/hpg_p2p.cuh).  Collective setup, nranks > 1:

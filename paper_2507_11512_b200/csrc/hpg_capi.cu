@@ -1,5 +1,7 @@
 // libhpgmxp.so: context, hierarchy build, and the extern "C" entry points
 // declared in include/hpgmxp.h.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -9,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "hpgmxp.h"
@@ -19,6 +22,7 @@
 #include "hpg_p2p.cuh"
 #include "hpg_wave.cuh"
 #include "hpg_lower.cuh"
+#include "hpg_tma.cuh"
 
 using hpg::Geom;
 
@@ -238,7 +242,10 @@ struct hpg_ctx {
   bool cgs_fused = true;
   bool general = false;  // some level uses an explicit (non-greedy) coloring
   bool graphs = true;    // replay captured V-cycles (single rank)
-  bool lower = true;       // zero sweeps stream only the strictly-lower part (hpg_lower.cuh)
+  // zero sweeps stream only the strictly-lower part (hpg_lower.cuh).  Off by
+  // default: it skips the products against z = 0 that the reference forms
+  // (smoother.py:95-112) and that the HPG-MxP flop model counts
+  bool lower = false;
   bool known_zero = true;  // zero sweeps skip loads of known zeros (same arithmetic)
   // sweeps as one dataflow kernel (hpg_wave.cuh) where the layout allows; bit 0:
   // fp64 sweeps, bit 1: fp32.  Measured at 256^3: fp64 sweep -9%, fp32 +19%
@@ -247,6 +254,18 @@ struct hpg_ctx {
   int wave_lag = 8;
   bool wave_coh = false;
   int wave_blocks[2] = {0, 0};
+  // bulk-copy pipelined persistent sweeps (hpg_tma.cuh); bit 0: fp64, bit 1: fp32,
+  // for levels with at least tma_min_rows rows
+  int tma = 3;
+  int64_t tma_min_rows = 1 << 18;
+  int tma_blocks[2] = {0, 0};
+  int tma_contig = 0;  // (persistent sweep) CTAs own contiguous row slabs of every colour block
+  int tma_sweep = 0;   // 1: the persistent whole-sweep kernel instead of per-pass launches
+  // per-pass kernel (rows * 100 + CTAs per SM) [fp64, fp32]; measured 256^3 level-0 sweeps
+  // (r02, tools/sweep_ab.py): fp32 64x16 479 us (256x5 with spills 699, 128x8 490),
+  // fp64 64x10 776 us (128x6 897, 64x12 796) vs 581 / 1032 us for k_gs_pass / the wave sweep
+  int tma_cfg[2] = {3220, 6416};  // fp64 32x20: 762 us
+  unsigned* sweep_done = nullptr;  // pass counters of the persistent sweep
   std::vector<GraphEntry> gcache;
   uint64_t gclock = 0;
   bool pdl = true;
@@ -313,6 +332,21 @@ cudaError_t launch_pdl(hpg_ctx* c, void (*k)(KArgs...), int grid, int block, Arg
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = 0;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = c->pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...);
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_smem(hpg_ctx* c, void (*k)(KArgs...), int grid, int block, size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = c->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -497,6 +531,171 @@ int gs_wave_launch(hpg_ctx* c, Level& L, const T* r, T* z, int zero) {
 }
 
 // One forward multicolor sweep (ref: smoother.py:78-114).  Multi-rank: the
+// Persistent bulk-copy pipelined sweep (hpg_tma.cuh): tile rows / ring depth
+template <typename T>
+struct TmaCfg;
+template <>
+struct TmaCfg<float> {
+  static constexpr int kRows = 256, kStages = 4;
+};
+template <>
+struct TmaCfg<double> {
+  static constexpr int kRows = 128, kStages = 4;
+};
+
+template <typename T>
+size_t tma_smem() {
+  return (size_t)TmaCfg<T>::kStages * hpg::TmaTile<T, TmaCfg<T>::kRows>::kBytes + 2 * TmaCfg<T>::kStages * 8;
+}
+
+template <typename T>
+bool tma_ok(hpg_ctx* c, const Level& L) {
+  if (!((c->tma >> (sizeof(T) == 4)) & 1) || L.n < c->tma_min_rows || c->tma_blocks[sizeof(T) == 4] <= 0) return false;
+  // tensor map: 16-byte aligned base and row pitch; every tile starts 16-byte aligned
+  // (tile starts are colour offsets plus multiples of 32 rows)
+  if ((L.ld * (int64_t)sizeof(T)) % 16 || ((uintptr_t)vals_of<T>(L)) % 16 || L.ld >= (int64_t{1} << 31)) return false;
+  if (L.ld < std::max(TmaCfg<T>::kRows, c->tma_cfg[sizeof(T) == 4] / 100)) return false;  // the box fits the tensor
+  for (int k = 0; k <= L.g.ncolors; ++k)
+    if ((L.g.off[k] * (int64_t)sizeof(T)) % 16) return false;
+  return true;
+}
+
+// The value planes [27][ld] of T as a 2-D tensor map, box {rows, 27}
+// (cuTensorMapEncodeTiled through the runtime's driver entry point: no -lcuda).
+template <typename T>
+int encode_value_map(hpg_ctx* c, const Level& L, int rows, CUtensorMap* map) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) return fail(HPG_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)L.ld, 27};
+  const cuuint64_t strides[1] = {(cuuint64_t)L.ld * sizeof(T)};
+  const cuuint32_t box[2] = {(cuuint32_t)rows, 27};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                      (void*)vals_of<T>(L), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HPG_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return HPG_OK;
+}
+
+void stencil_offsets(const hpg::Stencil& st, int col, int32_t* doff, uint32_t* kmask);
+
+template <typename T>
+int gs_sweep_tma(hpg_ctx* c, Level& L, const T* r, T* z, int zero) {
+  hpg::SweepPlan p;
+  memset(&p, 0, sizeof p);
+  int rc0 = encode_value_map<T>(c, L, TmaCfg<T>::kRows, &p.vmap);
+  if (rc0) return rc0;
+  p.cols = L.cols;
+  p.vals = vals_of<T>(L);
+  p.ld = L.ld;
+  p.ncolors = L.g.ncolors;
+  for (int k = 0; k <= L.g.ncolors; ++k) p.off[k] = L.g.off[k];
+  p.zero = zero;
+  p.rev_odd = c->gs_rev ? 1 : 0;
+  p.contiguous = c->tma_contig;
+  p.done = c->sweep_done;
+  p.st = stencil_of(c, L);
+  if (p.st.on)  // per-colour column offsets of implicit-index rows (see hpg_tma.cuh SweepPlan)
+    for (int col = 0; col < 8; ++col) stencil_offsets(p.st, col, p.doff[col], &p.kmask[col]);
+  constexpr int R = TmaCfg<T>::kRows, S = TmaCfg<T>::kStages;
+  CUDA_TRY(launch_pdl_smem(c, hpg::k_gs_sweep_tma<T, R, S>, c->tma_blocks[sizeof(T) == 4], 32 + R, tma_smem<T>(), p, r,
+                           z));
+  ++c->launches;
+  return HPG_OK;
+}
+
+// per-pass TMA-fed colour pass: (rows per CTA, CTAs per SM) chosen per precision
+// by the option "tma_cfg32" / "tma_cfg64" = rows * 100 + CTAs per SM
+#define HPG_PASS_CFGS(X) X(float, 256, 5) X(float, 256, 4) X(float, 128, 10) X(float, 128, 8) X(float, 64, 16) X(float, 32, 32) \
+  X(float, 64, 12) X(double, 128, 6) X(double, 128, 4) X(double, 64, 12) X(double, 64, 10) X(double, 64, 8) \
+  X(double, 32, 20)
+template <typename T, int R>
+size_t pass_smem() {
+  return (size_t)27 * R * sizeof(T) + 16;
+}
+
+// the per-colour constants of implicit-index rows (see hpg_tma.cuh SweepPlan)
+void stencil_offsets(const hpg::Stencil& st, int col, int32_t* doff, uint32_t* kmask) {
+  const int pxyz[3] = {(col >> st.bx) & 1, (col >> st.by) & 1, (col >> st.bz) & 1};
+  const int bits[3] = {st.bx, st.by, st.bz};
+  const int64_t stride[3] = {1, st.hx, st.hxy};
+  uint32_t km = 0;
+  for (int s = 0; s < 27; ++s) {
+    const int d[3] = {s % 3 - 1, (s / 3) % 3 - 1, s / 9 - 1};
+    int c2 = 0;
+    int64_t shift = 0;
+    for (int a = 0; a < 3; ++a) {
+      const int ax = pxyz[a] + d[a];  // in [-1, 2]
+      c2 |= (ax & 1) << bits[a];
+      shift += (int64_t)(ax >= 0 ? ax / 2 : -1) * stride[a];
+    }
+    doff[s] = (int32_t)((int64_t)(c2 - col) * st.n8 + shift);
+    if (c2 >= col) km |= 1u << s;
+  }
+  *kmask = km;
+}
+
+template <typename T, int R, int MB>
+int gs_pass_tma_t(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int rev) {
+  hpg::PassPlan p;
+  memset(&p, 0, sizeof p);
+  int rc0 = encode_value_map<T>(c, L, R, &p.vmap);
+  if (rc0) return rc0;
+  p.cols = L.cols;
+  p.ld = L.ld;
+  p.row0 = L.g.off[col];
+  p.nrows = L.g.off[col + 1] - p.row0;
+  p.known0 = zero ? p.row0 : -1;
+  p.rev = rev;
+  p.color = col;
+  p.st = stencil_of(c, L);
+  if (p.st.on) {
+    stencil_offsets(p.st, col, p.doff, &p.kmask);
+    if (!zero) p.kmask = 0;
+  }
+  if (p.nrows <= 0) return HPG_OK;
+  CUDA_TRY(launch_pdl_smem(c, hpg::k_gs_pass_tma<T, R, MB>, (int)cdiv(p.nrows, R), R, pass_smem<T, R>(), p, r, z));
+  ++c->launches;
+  return HPG_OK;
+}
+
+template <typename T>
+int gs_pass_tma(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int rev) {
+  const int code = c->tma_cfg[sizeof(T) == 4];
+#define HPG_PASS_CASE(TT, R, MB)                                                          \
+  if (std::is_same<T, TT>::value && code == R * 100 + MB)                                  \
+    return gs_pass_tma_t<TT, R, MB>(c, L, col, (const TT*)r, (TT*)z, zero, rev);
+  HPG_PASS_CFGS(HPG_PASS_CASE)
+#undef HPG_PASS_CASE
+  return fail(HPG_E_ARG, "unknown colour-pass configuration %d", code);
+}
+
+int pass_rows(int code) { return code / 100; }
+
+template <typename T>
+int tma_setup(hpg_ctx* c, int sms) {
+#define HPG_PASS_ATTR(TT, R, MB)                                                                         \
+  if (std::is_same<T, TT>::value)                                                                        \
+    CUDA_TRY(cudaFuncSetAttribute(hpg::k_gs_pass_tma<TT, R, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                  (int)pass_smem<TT, R>()));
+  HPG_PASS_CFGS(HPG_PASS_ATTR)
+#undef HPG_PASS_ATTR
+  constexpr int R = TmaCfg<T>::kRows, S = TmaCfg<T>::kStages;
+  auto fn = hpg::k_gs_sweep_tma<T, R, S>;
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem<T>()));
+  int per = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 32 + R, tma_smem<T>()));
+  c->tma_blocks[sizeof(T) == 4] = per * sms;
+  return HPG_OK;
+}
+
 // exchange of z overlaps color 0's interior rows, then color 0's boundary rows,
 // then colors 1.. (block-Jacobi across ranks: one exchange per sweep).
 template <typename T>
@@ -517,6 +716,24 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
     }
     for (int col = 0; col < L.g.ncolors; ++col)
       if ((rc = gs_lower_launch<T>(c, L, col, r, z))) return rc;
+    return HPG_OK;
+  }
+  if (tma_ok<T>(c, L) && !(overlapped(c, l) && !zero)) {
+    if (zero) {
+      if (L.n_ext > L.n) {  // zero initial guess: clear the halo tail; rows are all written
+        CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n_ext - L.n, 4)), 256, z + L.n, L.n_ext - L.n));
+        ++c->launches;
+      }
+      if (!c->known_zero) {
+        CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n, 4)), 256, z, L.n));
+        ++c->launches;
+      }
+    } else if ((rc = do_exchange(c, l, prec, z))) {
+      return rc;
+    }
+    if (c->tma_sweep) return gs_sweep_tma<T>(c, L, r, z, zero && c->known_zero);
+    for (int col = 0; col < L.g.ncolors; ++col)
+      if ((rc = gs_pass_tma<T>(c, L, col, r, z, zero && c->known_zero, c->gs_rev && (col & 1)))) return rc;
     return HPG_OK;
   }
   const bool use_wave = (c->wave >> (sizeof(T) == 4)) & 1 && L.wave_ok && L.n >= c->wave_min_rows && c->wave_blocks[sizeof(T) == 4] > 0 &&
@@ -1409,6 +1626,11 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     };
     c->wave_blocks[0] = std::min(occ(wave_fn<double>(true)), occ(wave_fn<double>(false)));
     c->wave_blocks[1] = std::min(occ(wave_fn<float>(true)), occ(wave_fn<float>(false)));
+    const char* tm = getenv("HPG_TMA");
+    if (tm) c->tma = atoi(tm);
+    const char* tr = getenv("HPG_TMA_MIN_ROWS");
+    if (tr) c->tma_min_rows = atoll(tr);
+    if (tma_setup<float>(c, sms) || tma_setup<double>(c, sms)) return bail(HPG_E_CUDA);
     const char* f = getenv("HPG_CGS_FUSED");
     c->cgs_fused = !(f && f[0] == '0');
     const char* sn = getenv("HPG_STENCIL");
@@ -1448,8 +1670,10 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
   // partials: [64][grid] for the per-pass kernels (nb CTAs) and the cooperative ones (<= 8 per SM)
   if (dmalloc((char**)&c->partial, (size_t)std::max(c->nb, 8 * sms) * 64 * 8, nullptr) ||
       dmalloc(&c->spmv_partial, c->spmv_partial_len * 8, nullptr) ||
-      dmalloc((char**)&c->scal, 512 * 8, nullptr) || dmalloc((char**)&c->gather, (size_t)nranks * 256 * 8, nullptr))
+      dmalloc((char**)&c->scal, 512 * 8, nullptr) || dmalloc((char**)&c->gather, (size_t)nranks * 256 * 8, nullptr) ||
+      dmalloc((char**)&c->sweep_done, 64 * 4, nullptr))
     return bail(HPG_E_CUDA);
+  if (cudaMemset(c->sweep_done, 0, 64 * 4) != cudaSuccess) return bail(fail(HPG_E_CUDA, "memset"));
   if (cudaMallocHost((void**)&c->pinned, 256 * 8) != cudaSuccess) return bail(fail(HPG_E_CUDA, "pinned alloc"));
   // nccl_uid == NULL: P2P-only context (every exchange and reduction over the
   // peer-memory path; lets several ranks share one GPU, where NCCL refuses)
@@ -1479,6 +1703,7 @@ int hpg_destroy(hpg_ctx* c) {
   if (c->sym) cudaFree(c->sym);
   if (c->d_peer) cudaFree(c->d_peer);
   if (c->done) cudaFree(c->done);
+  if (c->sweep_done) cudaFree(c->sweep_done);
   for (auto& e : c->gcache) cudaGraphExecDestroy(e.exec);
   for (auto e : c->events) cudaEventDestroy(e);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
@@ -1897,6 +2122,12 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   else if (!strcmp(key, "tail_cluster")) set_tail_cluster(c, (int)value);
   else if (!strcmp(key, "gs_rev")) c->gs_rev = value != 0;
   else if (!strcmp(key, "stencil")) c->stencil = value != 0;
+  else if (!strcmp(key, "tma")) c->tma = (int)value;
+  else if (!strcmp(key, "tma_min_rows")) c->tma_min_rows = value;
+  else if (!strcmp(key, "tma_contig")) c->tma_contig = (int)value;
+  else if (!strcmp(key, "tma_sweep")) c->tma_sweep = (int)value;
+  else if (!strcmp(key, "tma_cfg64")) c->tma_cfg[0] = (int)value;
+  else if (!strcmp(key, "tma_cfg32")) c->tma_cfg[1] = (int)value;
   else return fail(HPG_E_ARG, "unknown option %s", key);
   drop_graphs(c);
   return HPG_OK;

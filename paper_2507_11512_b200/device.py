@@ -14,7 +14,7 @@ INFO_KEYS = ("n", "n_ext", "nnz", "ncolors") + tuple(f"off{i}" for i in range(9)
     ("halo", "ld", "nneighbours", "device_bytes", "zero_sweep_slots", "stencil_rows", "stencil_lower")
 
 
-BOOL_DEFAULTS = {"stencil": 1, "lower": 1, "graphs": 1, "pdl": 1, "gs_rev": 1}
+BOOL_DEFAULTS = {"stencil": 1, "lower": 0, "graphs": 1, "pdl": 1, "gs_rev": 1}
 
 
 class Context:

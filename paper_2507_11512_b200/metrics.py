@@ -89,12 +89,21 @@ def gflops(flops, seconds):
 
 
 class Tally:
-    """Per-rank flops / model bytes / seconds per motif (ref: metrics.py:111-143)."""
+    """Per-rank flops / model bytes / seconds per motif (ref: metrics.py:111-143).
+
+    Beside the reference's model it keeps, per motif, the flops the kernels
+    actually EXECUTE (``exec_flops``: lower than the model only for the optional
+    strictly-lower zero-guess sweep) and the bytes they actually MOVE
+    (``moved_bytes``: the model minus the 4-B column indices that implicit-index
+    rows compute instead of loading, and the lower part only for that sweep).
+    """
 
     def __init__(self):
         self.flops = {m: 0 for m in MOTIFS}
         self.bytes = {m: 0 for m in MOTIFS}
         self.seconds = {m: 0.0 for m in MOTIFS}
+        self.exec_flops = {m: 0 for m in MOTIFS}
+        self.moved_bytes = {m: 0 for m in MOTIFS}
         # subsets of GS timed alone for the bench roofline: level-0 full sweeps
         # (k_gs_pass, model bytes) and level-0 zero-initial-guess sweeps
         # (k_gs_lower, the bytes that kernel streams)
@@ -105,10 +114,16 @@ class Tally:
         self.gs_level0z_bytes = 0
         self.gs_level0z_sweeps = 0
 
-    def add(self, kernel, dtype, motif=None, **sizes):
+    def add(self, kernel, dtype, motif=None, implicit_nnz=0, exec_flops=None, moved=None, **sizes):
+        """``implicit_nnz``: nonzeros whose column the kernel computes (no 4-B index
+        load); ``exec_flops`` / ``moved``: override both extra counts outright."""
         bucket = motif or kernel_motif(kernel)
-        self.flops[bucket] += count_flops(kernel, **sizes)
-        self.bytes[bucket] += count_bytes(kernel, np.dtype(dtype).itemsize, **sizes)
+        f = count_flops(kernel, **sizes)
+        b = count_bytes(kernel, np.dtype(dtype).itemsize, **sizes)
+        self.flops[bucket] += f
+        self.bytes[bucket] += b
+        self.exec_flops[bucket] += f if exec_flops is None else int(exec_flops)
+        self.moved_bytes[bucket] += (b - 4 * int(implicit_nnz)) if moved is None else int(moved)
 
     @contextmanager
     def timed(self, motif):
@@ -133,11 +148,19 @@ class Tally:
     def total_bytes(self):
         return sum(self.bytes.values())
 
+    def total_exec_flops(self):
+        return sum(self.exec_flops.values())
+
+    def total_moved_bytes(self):
+        return sum(self.moved_bytes.values())
+
     def reset(self):
         for m in MOTIFS:
             self.flops[m] = 0
             self.bytes[m] = 0
             self.seconds[m] = 0.0
+            self.exec_flops[m] = 0
+            self.moved_bytes[m] = 0
         self.gs_level0_seconds = 0.0
         self.gs_level0_bytes = 0
         self.gs_level0_sweeps = 0

@@ -85,21 +85,24 @@ class MgHierarchy:
 
 
 def count_vcycle(h, tally, dtype):
-    """Flop/byte accounting of one V-cycle, call by call as the reference tallies it."""
+    """Flop/byte accounting of one V-cycle, call by call as the reference tallies it
+    (model), plus the executed flops and moved bytes of the kernels that ran."""
     nl = len(h.levels)
     sw = h.sweeps
+    w = np.dtype(dtype).itemsize
     for lev in range(nl):
         A = h.levels[lev].A_hi
         last = lev == nl - 1
         sweeps = sw.nu_c if last else sw.nu1 + sw.nu2
         for k in range(sweeps):
-            tally.add("gs_sweep", dtype, nnz=A.nnz_total, n=A.n_rows)
+            zs = zero_sweep_counts(h, lev, w) if k == 0 else None
+            if zs is not None:  # strictly-lower zero-guess sweep (option "lower")
+                tally.add("gs_sweep", dtype, nnz=A.nnz_total, n=A.n_rows, exec_flops=zs[0], moved=zs[1])
+            else:
+                tally.add("gs_sweep", dtype, nnz=A.nnz_total, n=A.n_rows, implicit_nnz=A.implicit_nnz)
             if lev == 0 and hasattr(tally, "gs_level0_bytes"):
-                w = np.dtype(dtype).itemsize
-                if k == 0 and (last or sw.nu1 > 0) and h.ctx is not None:
-                    # the first sweep starts from z = 0: the strictly-lower kernel streams
-                    # its slots (index + value) and r, a_ii, z once each
-                    tally.gs_level0z_bytes += zero_sweep_bytes(h, w)
+                if zs is not None:
+                    tally.gs_level0z_bytes += zs[1]
                     tally.gs_level0z_sweeps += 1
                 else:
                     from .metrics import count_bytes
@@ -107,18 +110,41 @@ def count_vcycle(h, tally, dtype):
                     tally.gs_level0_sweeps += 1
         if not last:
             nxt = h.levels[lev + 1]
-            tally.add("restrict_fused", dtype, nnz=nxt.inject_nnz, n_c=nxt.A_hi.n_rows)
+            tally.add("restrict_fused", dtype, nnz=nxt.inject_nnz, n_c=nxt.A_hi.n_rows,
+                      implicit_nnz=restrict_implicit_nnz(h, lev))
             tally.add("prolong_add", dtype, n_c=nxt.A_hi.n_rows)
 
 
-def zero_sweep_bytes(h, w):
-    """Bytes one level-0 zero-initial-guess sweep streams (csrc/hpg_lower.cuh): lower
-    values, the column indices of the rows off the implicit-index path (pro rata), and
-    diagonal, r, z write plus the gathered z once."""
-    info = h.ctx.level_info(0)
+def zero_sweep_counts(h, lev, w):
+    """(executed flops, moved bytes) of a zero-initial-guess sweep at ``lev`` when it
+    runs the strictly-lower kernel (csrc/hpg_lower.cuh), else None (the sweep runs
+    the full color-pass kernel and forms every product like the reference, the
+    ones against z = 0 included)."""
+    if h.ctx is None or not h.ctx.option("lower"):
+        return None
+    info = h.ctx.level_info(lev)
     n, slots = info["n"], info["zero_sweep_slots"]
+    if slots >= 27 * n:
+        return None
     idx_rows = n - info["stencil_rows"] if info["stencil_lower"] and h.ctx.option("stencil") else n
-    return slots * w + 4 * slots * idx_rows // max(n, 1) + 4 * n * w
+    # W_c products + (r - sum) / a_ii per row; lower values (+ indices of indexed
+    # rows, pro rata), a_ii, r, z written, z gathered once
+    return 2 * slots + 2 * n, slots * w + 4 * slots * idx_rows // max(n, 1) + 4 * n * w
+
+
+def restrict_implicit_nnz(h, lev):
+    """Nonzeros of the injected fine rows on the implicit-index path (pro rata)."""
+    A = h.levels[lev].A_hi
+    nxt = h.levels[lev + 1]
+    if A.n_rows == 0:
+        return 0
+    return nxt.inject_nnz * (A.implicit_nnz // 27) // A.n_rows
+
+
+def zero_sweep_bytes(h, w):
+    """Bytes one level-0 zero-initial-guess sweep streams (see zero_sweep_counts)."""
+    zs = zero_sweep_counts(h, 0, w)
+    return zs[1] if zs is not None else full_sweep_moved_bytes(h, w)
 
 
 def full_sweep_moved_bytes(h, w):
@@ -218,7 +244,9 @@ def fused_residual_restrict(A_f, b_f, x_f, f2c=None, out=None, tally=None, n_c=N
         out = torch.empty(info["n"], dtype=A_f.torch_dtype, device=x_f.device)
     A_f.ctx.call("hpg_restrict", A_f.level, A_f.prec, _lib.ptr(b_f), _lib.ptr(x_f), _lib.ptr(out))
     if tally is not None:
-        tally.add("restrict_fused", A_f.dtype, nnz=_inject_nnz(A_f.domain), n_c=info["n"])
+        inj = _inject_nnz(A_f.domain)
+        tally.add("restrict_fused", A_f.dtype, nnz=inj, n_c=info["n"],
+                  implicit_nnz=inj * (A_f.implicit_nnz // 27) // max(A_f.n_rows, 1))
     return out
 
 

@@ -35,6 +35,14 @@ class EllMatrix:
         self._host = None
 
     @property
+    def implicit_nnz(self):
+        """Nonzeros of the rows whose columns the kernels compute in closed form
+        (implicit-index rows: 27 each, no column-index load) -- 0 with stencil off."""
+        if not self.ctx.option("stencil"):
+            return 0
+        return 27 * self.ctx.level_info(self.level)["stencil_rows"]
+
+    @property
     def dtype(self):
         return np.dtype(np.float32 if self.prec == _lib.F32 else np.float64)
 

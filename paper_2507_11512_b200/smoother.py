@@ -42,4 +42,14 @@ def forward_gs_sweep(A, r, z, coloring=None, plan=None, world=None, rank=0,
         raise TypeError(f"GS sweep operands must be {A.torch_dtype}")
     A.ctx.call("hpg_gs_sweep", A.level, A.prec, _lib.ptr(r), _lib.ptr(z), int(bool(z_is_zero)))
     if tally is not None:
-        tally.add("gs_sweep", A.dtype, nnz=A.nnz_total, n=A.n_rows)
+        zs = None
+        if z_is_zero and A.ctx.option("lower"):
+            from .multigrid import zero_sweep_counts
+
+            class _H:  # zero_sweep_counts needs only the context
+                ctx = A.ctx
+            zs = zero_sweep_counts(_H, A.level, A.dtype.itemsize)
+        if zs is not None:
+            tally.add("gs_sweep", A.dtype, nnz=A.nnz_total, n=A.n_rows, exec_flops=zs[0], moved=zs[1])
+        else:
+            tally.add("gs_sweep", A.dtype, nnz=A.nnz_total, n=A.n_rows, implicit_nnz=A.implicit_nnz)

@@ -382,7 +382,8 @@ def test_nonuniform_boxes_vcycle_bitwise_vs_oracle(dims):
 
 
 def test_execution_variants_agree_bitwise():
-    """Tuning switches never change results: the persistent V-cycle tail kernel
+    """Tuning switches never change results: the bulk-copy pipelined persistent
+    sweep (hpg_tma.cuh, forced onto every level), the persistent V-cycle tail kernel
     (cooperative grid, or one 16- / 8-CTA cluster), backwards odd-color passes,
     CUDA-graph replay, PDL, the known-zero sweep, the dataflow (wave) sweep and
     the strictly-lower zero sweep give the same V-cycle bits in both precisions; the host-pipelined and plain
@@ -407,9 +408,8 @@ def test_execution_variants_agree_bitwise():
     # really executed (checked through the eager launch counts), with graph
     # capture on and off
     ctx.set_option("graphs", 0)
-    base = launches_per_vcycle()
-    variants = (("tail_rows", 1 << 30), ("tail_cluster", 16), ("tail_cluster", 8), ("gs_rev", 1),
-                ("pdl", 0), ("known_zero", 0), ("wave", 0), ("lower", 0))
+    variants = (("tma_min_rows", 0), ("tail_rows", 1 << 30), ("tail_cluster", 16), ("tail_cluster", 8),
+                ("gs_rev", 1), ("pdl", 0), ("known_zero", 0), ("wave", 0), ("lower", 1), ("tma", 0))
     for graphs in (0, 1):
         for key, val in variants:
             ctx.set_option("graphs", graphs)
@@ -418,15 +418,19 @@ def test_execution_variants_agree_bitwise():
                 np.testing.assert_array_equal(h.apply(r).cpu().numpy(), ref, err_msg=f"{key}={val} graphs={graphs}")
             if key == "tail_rows" and graphs == 0:
                 # the whole V-cycle below the finest level runs in the tail kernel
-                assert launches_per_vcycle() < base
+                with_tail = launches_per_vcycle()
+                ctx.set_option("tail_rows", 0)
+                without = launches_per_vcycle()
+                ctx.set_option("tail_rows", val)
+                assert with_tail < without, (with_tail, without)
         for key, val in variants:  # back to the defaults for the next round
             ctx.set_option(key, {"tail_rows": 0, "tail_cluster": 0, "gs_rev": 0, "pdl": 1, "known_zero": 1,
-                                 "wave": 3, "lower": 1}[key])
+                                 "wave": 3, "lower": 0, "tma": 3, "tma_min_rows": 1 << 18}[key])
     ctx.set_option("graphs", 1)
     ctx.set_option("known_zero", 1)
     ctx.set_option("known_zero", 1)
     ctx.set_option("wave", 1)
-    ctx.set_option("lower", 1)
+    ctx.set_option("lower", 0)
     ctx.set_option("tail_rows", 0)
     ctx.set_option("tail_cluster", 0)
     ctx.set_option("gs_rev", 0)
@@ -521,7 +525,7 @@ def test_full_size_properties():
             z = torch.full((ne,), float("nan"), dtype=dt, device="cuda")
             forward_gs_sweep(A, rr, z, z_is_zero=True)
             zs.append(z[:n].clone())
-        ctx.set_option("lower", 1)
+        ctx.set_option("lower", 0)
         assert torch.equal(zs[0], zs[1])
         ref = h.apply(rr).clone()
         for key, val in (("graphs", 0), ("gs_rev", 0), ("pdl", 0), ("wave", 0), ("stencil", 0)):
