@@ -23,6 +23,7 @@
 #include "hpg_wave.cuh"
 #include "hpg_lower.cuh"
 #include "hpg_tma.cuh"
+#include "hpg_brick.cuh"
 
 using hpg::Geom;
 
@@ -264,7 +265,14 @@ struct hpg_ctx {
   // per-pass kernel (rows * 100 + CTAs per SM) [fp64, fp32]; measured 256^3 level-0 sweeps
   // (r02, tools/sweep_ab.py): fp32 64x16 479 us (256x5 with spills 699, 128x8 490),
   // fp64 64x10 776 us (128x6 897, 64x12 796) vs 581 / 1032 us for k_gs_pass / the wave sweep
-  int tma_cfg[2] = {3220, 6416};  // fp64 32x20: 762 us
+  int tma_cfg[2] = {3220, 6416};
+  // brick passes (hpg_brick.cuh): bit 0 fp64, bit 1 fp32; (rows * 100 + CTAs per SM).
+  // Off: measured slower (r02, fp32 level-0 sweep 638 us at 128x8 vs 480 for the
+  // tma pass) -- each CTA's neighbour-z boxes can only be requested after the PDL
+  // wait and their latency is exposed per CTA
+  int brick = 0;
+  int brick_cfg[2] = {12804, 25605};
+  size_t brick_smem_max = 64 * 1024;  // fp64 32x20: 762 us
   unsigned* sweep_done = nullptr;  // pass counters of the persistent sweep
   std::vector<GraphEntry> gcache;
   uint64_t gclock = 0;
@@ -679,8 +687,130 @@ int gs_pass_tma(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int r
 
 int pass_rows(int code) { return code / 100; }
 
+// ---- brick colour pass (hpg_brick.cuh): values AND neighbour z staged by tensor copies
+#define HPG_BRICK_CFGS(X) X(float, 256, 5) X(float, 256, 4) X(float, 128, 8) X(double, 128, 4) X(double, 128, 3) \
+  X(double, 64, 8)
+
+template <typename T>
+PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder(hpg_ctx* c) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  return encode;
+}
+
+// the brick tiling applies: implicit-index layout, ROWS whole x-lines of one plane,
+// every box within the tensor-copy limits
+template <typename T>
+bool brick_ok(hpg_ctx* c, const Level& L, int rows) {
+  const hpg::Stencil st = stencil_of(c, L);
+  if (!st.on || !((c->brick >> (sizeof(T) == 4)) & 1)) return false;
+  const int pad = 16 / (int)sizeof(T);
+  const int hx = (int)st.hx, hy = (int)st.hy;
+  if (hx % pad || rows % hx || hy % (rows / hx) || hx + pad > 256 || rows / hx + 1 > 256) return false;
+  return true;
+}
+
+template <typename T, int R, int MB>
+int gs_pass_brick_t(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int rev) {
+  hpg::BrickPlan p;
+  memset(&p, 0, sizeof p);
+  int rc0 = encode_value_map<T>(c, L, R, &p.vmap);
+  if (rc0) return rc0;
+  const hpg::Stencil st = stencil_of(c, L);
+  const int w = (int)sizeof(T), pad = 16 / w;
+  const int hx = (int)st.hx, hy = (int)st.hy, hz = (int)(st.n8 / st.hxy), BY = R / hx;
+  p.cols = L.cols;
+  p.ld = L.ld;
+  p.row0 = L.g.off[col];
+  p.nrows = L.g.off[col + 1] - p.row0;
+  p.known0 = zero ? p.row0 : -1;
+  p.rev = rev;
+  p.color = col;
+  p.hx = hx;
+  p.hxy = (int)st.hxy;
+  p.pad = pad;
+  p.st = st;
+  const int par[3] = {(col >> st.bx) & 1, (col >> st.by) & 1, (col >> st.bz) & 1};
+  const int bits[3] = {st.bx, st.by, st.bz};
+  int xe[8], ye[8];
+  int off = 0;
+  auto encode = tensor_encoder<T>(c);
+  if (!encode) return fail(HPG_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  for (int am = 1; am < 8; ++am) {
+    const int xb = am & 1, yb = (am >> 1) & 1, zb = (am >> 2) & 1;
+    xe[am] = hx + (xb ? pad : 0);
+    ye[am] = BY + yb;
+    const int ze = 1 + zb;
+    // the innermost start coordinate of a tensor copy must be 16-byte aligned (x = -1
+    // faults: tools/tma4d_test.cu), so a box reaching one column left starts at -pad
+    p.box_x[am] = (xb && par[0] == 0) ? -pad : 0;
+    p.box_y[am] = (yb && par[1] == 0) ? -1 : 0;
+    p.box_z[am] = (zb && par[2] == 0) ? -1 : 0;
+    p.box_c[am] = col ^ ((xb << bits[0]) | (yb << bits[1]) | (zb << bits[2]));
+    p.box_off[am] = off;
+    p.box_bytes[am] = (uint32_t)(xe[am] * ye[am] * ze * w);
+    off += (xe[am] * ye[am] * ze * w + 127) / 128 * 128 / w;
+    if (!zero || p.box_c[am] < col) p.load_mask |= 1u << am;
+    // X extent hx + pad: a box may not be wider than its tensor (entries past hx alias the next
+    // line and are never read by an interior row)
+    const cuuint64_t dims[4] = {(cuuint64_t)(hx + pad), (cuuint64_t)hy, (cuuint64_t)hz, 8};
+    const cuuint64_t strides[3] = {(cuuint64_t)hx * w, (cuuint64_t)st.hxy * w, (cuuint64_t)st.n8 * w};
+    const cuuint32_t box[4] = {(cuuint32_t)xe[am], (cuuint32_t)ye[am], (cuuint32_t)ze, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult er = encode(&p.zmap[am], w == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                         (void*)z, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (er != CUDA_SUCCESS) return fail(HPG_E_CUDA, "z tensor map encode failed (%d)", (int)er);
+  }
+  p.box_off[0] = off;  // end of the boxes: the mbarriers follow
+  for (int s = 0; s < 27; ++s) {
+    const int d[3] = {s % 3 - 1, (s / 3) % 3 - 1, s / 9 - 1};
+    const int am = (d[0] != 0) | ((d[1] != 0) << 1) | ((d[2] != 0) << 2);
+    if (!am) continue;  // the diagonal
+    int e[3];
+    for (int a = 0; a < 3; ++a) {
+      const int ax = par[a] + d[a];
+      e[a] = ax >= 0 ? ax / 2 : -1;
+    }
+    const int xl = e[0] - p.box_x[am], yl = e[1] - p.box_y[am], zl = e[2] - p.box_z[am];
+    p.sconst[s] = p.box_off[am] + xl + xe[am] * yl + xe[am] * ye[am] * zl;
+    if (am & 1) p.xsel |= 1u << s;
+    if (zero && p.box_c[am] >= col) p.kmask |= 1u << s;
+  }
+  if (p.nrows <= 0) return HPG_OK;
+  const size_t zoff = (hpg::BrickSmem<T, R>::kValBytes + 127) / 128 * 128;
+  const size_t smem = zoff + (size_t)off * w + 16;
+  if (smem > c->brick_smem_max) return fail(HPG_E_ARG, "brick tile needs %zu B of shared memory", smem);
+  CUDA_TRY(launch_pdl_smem(c, hpg::k_gs_pass_brick<T, R, MB>, (int)cdiv(p.nrows, R), R, smem, p, r, z, zoff));
+  ++c->launches;
+  return HPG_OK;
+}
+
+template <typename T>
+int gs_pass_brick(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int rev) {
+  const int code = c->brick_cfg[sizeof(T) == 4];
+#define HPG_BRICK_CASE(TT, R, MB)                                                     \
+  if (std::is_same<T, TT>::value && code == R * 100 + MB)                              \
+    return gs_pass_brick_t<TT, R, MB>(c, L, col, (const TT*)r, (TT*)z, zero, rev);
+  HPG_BRICK_CFGS(HPG_BRICK_CASE)
+#undef HPG_BRICK_CASE
+  return fail(HPG_E_ARG, "unknown brick-pass configuration %d", code);
+}
+
 template <typename T>
 int tma_setup(hpg_ctx* c, int sms) {
+#define HPG_BRICK_ATTR(TT, R, MB)                                                                           \
+  if (std::is_same<T, TT>::value)                                                                           \
+    CUDA_TRY(cudaFuncSetAttribute(hpg::k_gs_pass_brick<TT, R, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                  (int)c->brick_smem_max));
+  HPG_BRICK_CFGS(HPG_BRICK_ATTR)
+#undef HPG_BRICK_ATTR
 #define HPG_PASS_ATTR(TT, R, MB)                                                                         \
   if (std::is_same<T, TT>::value)                                                                        \
     CUDA_TRY(cudaFuncSetAttribute(hpg::k_gs_pass_tma<TT, R, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -732,8 +862,11 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
       return rc;
     }
     if (c->tma_sweep) return gs_sweep_tma<T>(c, L, r, z, zero && c->known_zero);
-    for (int col = 0; col < L.g.ncolors; ++col)
-      if ((rc = gs_pass_tma<T>(c, L, col, r, z, zero && c->known_zero, c->gs_rev && (col & 1)))) return rc;
+    const bool brick = brick_ok<T>(c, L, c->brick_cfg[sizeof(T) == 4] / 100);
+    for (int col = 0; col < L.g.ncolors; ++col) {
+      const int zz = zero && c->known_zero, rv = c->gs_rev && (col & 1);
+      if ((rc = brick ? gs_pass_brick<T>(c, L, col, r, z, zz, rv) : gs_pass_tma<T>(c, L, col, r, z, zz, rv))) return rc;
+    }
     return HPG_OK;
   }
   const bool use_wave = (c->wave >> (sizeof(T) == 4)) & 1 && L.wave_ok && L.n >= c->wave_min_rows && c->wave_blocks[sizeof(T) == 4] > 0 &&
@@ -2128,6 +2261,9 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   else if (!strcmp(key, "tma_sweep")) c->tma_sweep = (int)value;
   else if (!strcmp(key, "tma_cfg64")) c->tma_cfg[0] = (int)value;
   else if (!strcmp(key, "tma_cfg32")) c->tma_cfg[1] = (int)value;
+  else if (!strcmp(key, "brick")) c->brick = (int)value;
+  else if (!strcmp(key, "brick_cfg64")) c->brick_cfg[0] = (int)value;
+  else if (!strcmp(key, "brick_cfg32")) c->brick_cfg[1] = (int)value;
   else return fail(HPG_E_ARG, "unknown option %s", key);
   drop_graphs(c);
   return HPG_OK;
