@@ -272,7 +272,11 @@ struct hpg_ctx {
   // wait and their latency is exposed per CTA
   int brick = 0;
   int brick_cfg[2] = {12804, 25605};
-  size_t brick_smem_max = 64 * 1024;  // fp64 32x20: 762 us
+  size_t brick_smem_max = 64 * 1024;
+  // SpMV / fp64 residual with staged values: bit 0 fp64, bit 1 fp32; configurations
+  int spmv_tma = 3;
+  int spmv_cfg[2] = {3220, 6416};  // measured r02: fp32 SpMV 446 -> 417 us, fp64 683 -> 667 us
+  int resid_cfg = 6410;  // measured r02: residual 867 -> 800 us (32x20: 913)  // fp64 32x20: 762 us
   unsigned* sweep_done = nullptr;  // pass counters of the persistent sweep
   std::vector<GraphEntry> gcache;
   uint64_t gclock = 0;
@@ -688,6 +692,8 @@ int gs_pass_tma(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int r
 int pass_rows(int code) { return code / 100; }
 
 // ---- brick colour pass (hpg_brick.cuh): values AND neighbour z staged by tensor copies
+#define HPG_SPMV_CFGS(X) X(float, 64, 16, 0) X(float, 128, 8, 0) X(float, 32, 32, 0) X(double, 32, 20, 0) \
+  X(double, 64, 10, 0) X(double, 64, 8, 0) X(double, 32, 20, 1) X(double, 64, 10, 1) X(double, 64, 8, 1)
 #define HPG_BRICK_CFGS(X) X(float, 256, 5) X(float, 256, 4) X(float, 128, 8) X(double, 128, 4) X(double, 128, 3) \
   X(double, 64, 8)
 
@@ -811,6 +817,12 @@ int tma_setup(hpg_ctx* c, int sms) {
                                   (int)c->brick_smem_max));
   HPG_BRICK_CFGS(HPG_BRICK_ATTR)
 #undef HPG_BRICK_ATTR
+#define HPG_SPMV_ATTR(TT, R, MB, MD)                                                                   \
+  if (std::is_same<T, TT>::value)                                                                      \
+    CUDA_TRY(cudaFuncSetAttribute(hpg::k_spmv_tma<TT, R, MB, MD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                  (int)((size_t)27 * R * sizeof(TT) + 16)));
+  HPG_SPMV_CFGS(HPG_SPMV_ATTR)
+#undef HPG_SPMV_ATTR
 #define HPG_PASS_ATTR(TT, R, MB)                                                                         \
   if (std::is_same<T, TT>::value)                                                                        \
     CUDA_TRY(cudaFuncSetAttribute(hpg::k_gs_pass_tma<TT, R, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -1550,8 +1562,57 @@ int check_level(hpg_ctx* c, int l) {
   return l >= 0 && l < c->nlev ? HPG_OK : fail(HPG_E_ARG, "level %d out of range", l);
 }
 
+// ---- SpMV / residual with tensor-copy staged values (hpg_tma.cuh k_spmv_tma)
+
+template <typename T, int R, int MB, int MODE>
+int spmv_tma_t(hpg_ctx* c, Level& L, const T* x, const T* b, T* y, double* partial, int64_t* nblocks) {
+  hpg::SpmvPlan p;
+  memset(&p, 0, sizeof p);
+  int rc0 = encode_value_map<T>(c, L, R, &p.vmap);
+  if (rc0) return rc0;
+  p.cols = L.cols;
+  p.ld = L.ld;
+  p.n = L.n;
+  p.st = stencil_of(c, L);
+  if (p.st.on && p.st.n8 % R == 0) {
+    p.n8 = p.st.n8;
+    uint32_t km;
+    for (int col = 0; col < 8; ++col) stencil_offsets(p.st, col, p.doff[col], &km);
+  } else {
+    p.st.on = 0;
+  }
+  const int ilv = std::max(1, c->spmv_ilv[sizeof(T) == 4]);
+  p.ilv = ilv;
+  const int64_t nbk = cdiv(L.n, R);
+  if (nblocks) *nblocks = nbk;
+  const int grid = (int)(cdiv(nbk, ilv) * ilv);
+  CUDA_TRY(launch_pdl_smem(c, hpg::k_spmv_tma<T, R, MB, MODE>, grid, R, (size_t)27 * R * sizeof(T) + 16, p, x, b, y,
+                           partial));
+  ++c->launches;
+  return HPG_OK;
+}
+
+template <typename T, int MODE>
+int spmv_tma(hpg_ctx* c, Level& L, const T* x, const T* b, T* y, double* partial, int64_t* nblocks) {
+  const int code = MODE == 1 ? c->resid_cfg : c->spmv_cfg[sizeof(T) == 4];
+#define HPG_SPMV_CASE(TT, R, MB, MD)                                                                  \
+  if (std::is_same<T, TT>::value && MODE == MD && code == R * 100 + MB)                                \
+    return spmv_tma_t<TT, R, MB, MD>(c, L, (const TT*)x, (const TT*)b, (TT*)y, partial, nblocks);
+  HPG_SPMV_CFGS(HPG_SPMV_CASE)
+#undef HPG_SPMV_CASE
+  return fail(HPG_E_ARG, "unknown SpMV configuration %d", code);
+}
+
+template <typename T>
+bool spmv_tma_ok(hpg_ctx* c, const Level& L, int rows) {
+  return ((c->spmv_tma >> (sizeof(T) == 4)) & 1) && L.n >= c->tma_min_rows && L.ld >= rows &&
+         (L.ld * (int64_t)sizeof(T)) % 16 == 0 && ((uintptr_t)vals_of<T>(L)) % 16 == 0 && L.ld < (int64_t{1} << 31);
+}
+
 template <typename T>
 int spmv_launch(hpg_ctx* c, Level& L, int64_t cnt, const T* x, T* y, const uint8_t* skip, const int32_t* list) {
+  if (!skip && !list && cnt == L.n && spmv_tma_ok<T>(c, L, c->spmv_cfg[sizeof(T) == 4] / 100))
+    return spmv_tma<T, 0>(c, L, x, nullptr, y, nullptr, nullptr);
   if (skip || list)
     CUDA_TRY(launch_pdl(c, hpg::k_spmv<T, 0, true>, grid_for(cnt), 256, (const int32_t*)L.cols,
                         (const T*)vals_of<T>(L), L.ld, (int64_t)0, cnt, x, (const T*)nullptr, y, (double*)nullptr,
@@ -1799,7 +1860,7 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     if (tc) set_tail_cluster(c, atoi(tc));
   }
   c->nb = (int)std::min<int64_t>(8 * sms, std::max<int64_t>(1, cdiv(c->lev[0].n, 256)));
-  c->spmv_partial_len = grid_for(c->lev[0].n);
+  c->spmv_partial_len = cdiv(c->lev[0].n, 32);  // one partial per row tile (>= 32 rows)
   // partials: [64][grid] for the per-pass kernels (nb CTAs) and the cooperative ones (<= 8 per SM)
   if (dmalloc((char**)&c->partial, (size_t)std::max(c->nb, 8 * sms) * 64 * 8, nullptr) ||
       dmalloc(&c->spmv_partial, c->spmv_partial_len * 8, nullptr) ||
@@ -2087,13 +2148,18 @@ int hpg_residual(hpg_ctx* c, const double* b, double* x, double* r, double* rho2
   if ((rc = do_exchange(c, 0, HPG_F64, x))) return rc;
   Level& L = c->lev[0];
   double* scal = (double*)c->scal;
-  const int nbk = grid_for(L.n);
-  const int ilv = std::max(1, c->spmv_ilv[0]);
-  hpg::k_spmv<double, 1><<<(int)(cdiv(nbk, ilv) * ilv), 256, 0, c->stream>>>(
-      L.cols, L.v64, L.ld, 0, L.n, x, b, r, c->spmv_partial, nullptr, nullptr, stencil_of(c, L), ilv);
-  hpg::k_fold<double><<<1, 1024, 0, c->stream>>>(c->spmv_partial, nbk, 1, scal + 200, 0);
+  int64_t nbk = grid_for(L.n);
+  if (spmv_tma_ok<double>(c, L, c->resid_cfg / 100) && cdiv(L.n, c->resid_cfg / 100) <= c->spmv_partial_len) {
+    if ((rc = spmv_tma<double, 1>(c, L, x, b, r, c->spmv_partial, &nbk))) return rc;
+  } else {
+    const int ilv = std::max(1, c->spmv_ilv[0]);
+    hpg::k_spmv<double, 1><<<(int)(cdiv(nbk, ilv) * ilv), 256, 0, c->stream>>>(
+        L.cols, L.v64, L.ld, 0, L.n, x, b, r, c->spmv_partial, nullptr, nullptr, stencil_of(c, L), ilv);
+    ++c->launches;
+  }
+  hpg::k_fold<double><<<1, 1024, 0, c->stream>>>(c->spmv_partial, (int)nbk, 1, scal + 200, 0);
   LAUNCH_CHECK();
-  c->launches += 2;
+  c->launches += 1;
   if ((rc = allreduce_scal<double>(c, scal + 200, 1))) return rc;
   }
   CUDA_TRY(cudaMemcpyAsync(c->pinned + 200, (double*)c->scal + 200, 8, cudaMemcpyDeviceToHost, c->stream));
@@ -2262,6 +2328,10 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   else if (!strcmp(key, "tma_cfg64")) c->tma_cfg[0] = (int)value;
   else if (!strcmp(key, "tma_cfg32")) c->tma_cfg[1] = (int)value;
   else if (!strcmp(key, "brick")) c->brick = (int)value;
+  else if (!strcmp(key, "spmv_tma")) c->spmv_tma = (int)value;
+  else if (!strcmp(key, "spmv_cfg64")) c->spmv_cfg[0] = (int)value;
+  else if (!strcmp(key, "spmv_cfg32")) c->spmv_cfg[1] = (int)value;
+  else if (!strcmp(key, "resid_cfg")) c->resid_cfg = (int)value;
   else if (!strcmp(key, "brick_cfg64")) c->brick_cfg[0] = (int)value;
   else if (!strcmp(key, "brick_cfg32")) c->brick_cfg[1] = (int)value;
   else return fail(HPG_E_ARG, "unknown option %s", key);

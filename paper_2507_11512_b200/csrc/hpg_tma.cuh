@@ -381,4 +381,84 @@ __global__ void __launch_bounds__(ROWS, MINB) k_gs_pass_tma(const __grid_constan
   z[i] = div_rn(sub_rn(ri, acc), d);
 }
 
+// ---------------------------------------------------------------------------
+// SpMV (MODE 0: y = A x) and the fp64 outer residual (MODE 1: y = b - A x and a
+// per-CTA partial of sum y^2) with the same staging as k_gs_pass_tma: one
+// tensor copy of the tile's value planes before the PDL wait, the row's 27
+// gathers in registers, the slot-ordered sum (ref: krylov.py:76-107, 215-226).
+// ilv > 1: consecutive CTAs take the same tile position in ilv equal segments
+// of the rows (the colour blocks) so the x lines they gather are shared in L2.
+struct SpmvPlan {
+  CUtensorMap vmap;     // value planes [27][ld] of T, box {ROWS, 27}
+  const int32_t* cols;  // face rows only
+  int64_t ld, n;
+  int64_t n8;           // implicit-index rows: colour block size (a multiple of ROWS)
+  int ilv;
+  int32_t doff[8][27];  // implicit-index rows of colour c: slot s reads column i + doff[c][s]
+  Stencil st;
+};
+
+template <typename T, int ROWS, int MINB, int MODE>
+__global__ void __launch_bounds__(ROWS, MINB) k_spmv_tma(const __grid_constant__ SpmvPlan p, const T* __restrict__ x,
+                                                         const T* __restrict__ b, T* __restrict__ y,
+                                                         double* __restrict__ partial) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* sv = (T*)smem;
+  uint64_t* bar = (uint64_t*)(smem + (size_t)27 * ROWS * sizeof(T));
+  int64_t blk = blockIdx.x;
+  if (p.ilv > 1) blk = (int64_t)(blockIdx.x % p.ilv) * (gridDim.x / p.ilv) + blockIdx.x / p.ilv;
+  const int64_t tile0 = blk * ROWS;
+  if (tile0 >= p.n) return;  // (grid padded to a multiple of ilv)
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(bar, (uint32_t)(27 * ROWS * sizeof(T)));
+    tma_g2s_2d(sv, &p.vmap, (int)tile0, 0, bar, evict_first_policy());
+  }
+  pdl_trigger();
+  __syncthreads();
+  pdl_wait();  // x (and b) come from the predecessors
+  const int t = threadIdx.x;
+  const int64_t i = tile0 + t;
+  double sq = 0.0;
+  if (i < p.n) {
+    T g[27];
+    const int col = p.st.on ? (int)(tile0 / p.n8) : 0;
+    if (p.st.on && st_interior(p.st, i, col)) {
+      const T* xi = x + i;
+#pragma unroll
+      for (int s = 0; s < 27; ++s) g[s] = xi[p.doff[col][s]];
+    } else {
+#pragma unroll
+      for (int s = 0; s < 27; ++s) {
+        const int32_t cc = __ldg(p.cols + s * p.ld + i);
+        g[s] = x[cc < 0 ? ~cc : cc];
+      }
+    }
+    mbar_wait(bar, 0);
+    T acc = T(0);
+#pragma unroll
+    for (int s = 0; s < 27; ++s) acc = add_rn(acc, mul_rn(sv[s * ROWS + t], g[s]));
+    if (MODE == 0) {
+      y[i] = acc;
+    } else {
+      const T rr = sub_rn(b[i], acc);
+      y[i] = rr;
+      sq = (double)rr * (double)rr;
+    }
+  }
+  if (MODE == 1) {  // deterministic CTA reduction, indexed by the row tile
+    __shared__ double red[ROWS / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if ((t & 31) == 0) red[t >> 5] = sq;
+    __syncthreads();
+    if (t == 0) {
+      double a = 0.0;
+      for (int w = 0; w < ROWS / 32; ++w) a += red[w];
+      partial[blk] = a;
+    }
+  }
+}
+
 }  // namespace hpg

@@ -45,7 +45,18 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps * 1e3  # us
 
+    import ctypes as C
+    from paper_2507_11512_b200 import _lib
+    from paper_2507_11512_b200.krylov import spmv
+    x32 = torch.randn(ne, device="cuda", generator=gen)
+    x64 = x32.double()
+    y32 = torch.empty(n, device="cuda")
+    y64 = torch.empty(n, device="cuda", dtype=torch.float64)
+    rho2 = C.c_double()
     cases = {
+        "spmv_f32": lambda: spmv(lv.A_lo, x32, out=y32),
+        "spmv_f64": lambda: spmv(lv.A_hi, x64, out=y64),
+        "resid_f64": lambda: ctx.call("hpg_residual", _lib.ptr(b), _lib.ptr(x64), _lib.ptr(y64), C.byref(rho2)),
         "sweep_f32": lambda: forward_gs_sweep(lv.A_lo, r32, z32),
         "zero_sweep_f32": lambda: forward_gs_sweep(lv.A_lo, r32, z32, z_is_zero=True),
         "sweep_f64": lambda: forward_gs_sweep(lv.A_hi, r64, z64),
@@ -69,7 +80,10 @@ def main():
         forward_gs_sweep(lv.A_lo, r32, z32)
         forward_gs_sweep(lv.A_hi, r64, z64, z_is_zero=True)
         forward_gs_sweep(lv.A_hi, r64, z64)
-        bits[v] = (z32.clone(), z64.clone(), hier.apply(r32).clone(), hier.apply(r64).clone())
+        sp = (spmv(lv.A_lo, x32, out=y32).clone(), spmv(lv.A_hi, x64, out=y64).clone())
+        ctx.call("hpg_residual", _lib.ptr(b), _lib.ptr(x64), _lib.ptr(y64), C.byref(rho2))
+        bits[v] = (z32.clone(), z64.clone(), hier.apply(r32).clone(), hier.apply(r64).clone()) + sp + (y64.clone(),)
+        out.setdefault("rho2", []).append(rho2.value)
     ref = bits[vals[0]]
     out["bitwise_equal"] = all(all(torch.equal(x, y) for x, y in zip(ref, bits[v])) for v in vals[1:])
     hier.close()
