@@ -129,3 +129,20 @@ def ptr(t):
 
 def dptr(a):
     return a.ctypes.data_as(_dp)
+
+
+def on_device(v, torch_dtype, device):
+    """(device tensor, host array or None): a host numpy vector argument of the
+    reference's array API is copied to the device; the caller copies results
+    back into the host array (in-place contracts) -- compute stays on the GPU."""
+    import numpy as np
+    import torch
+    if isinstance(v, np.ndarray):
+        return torch.from_numpy(np.ascontiguousarray(v)).to(device=device, dtype=torch_dtype), v
+    return v, None
+
+
+def back_to_host(t, host):
+    """Copy a device result into the caller's host array (if it gave one)."""
+    if host is not None:
+        host[...] = t.cpu().numpy().astype(host.dtype, copy=False)

@@ -118,3 +118,56 @@ def color(A_or_dims, strategy="greedy", seed=0):
     if strategy == "jpl":
         return jpl_coloring(*dims, seed=seed)
     raise ValueError(f"unknown coloring strategy: {strategy!r}")
+
+
+def identity_coloring(n):
+    """One colour, natural order (ref: coloring.py:84-88)."""
+    return Coloring(color=np.zeros(n, dtype=np.int32), num_colors=1,
+                    color_offsets=np.array([0, n], dtype=np.int64),
+                    perm=np.arange(n), iperm=np.arange(n))
+
+
+def check_coloring(A, coloring):
+    """True iff no two locally coupled rows share a colour (ref: coloring.py:91-98).
+    ``A`` (or a domain / local dims) gives the local box; rows in natural order."""
+    dims = getattr(A, "local_dims", A)
+    lx, ly, lz = dims
+    n = lx * ly * lz
+    rows = np.arange(n, dtype=np.int64)
+    nb = _local_neighbours(lx, ly, lz, rows)
+    col = np.asarray(coloring.color)
+    ok = nb >= 0
+    return not np.any(ok & (col[np.where(ok, nb, 0)] == col[:, None]))
+
+
+def permute_system(A, vectors, coloring):
+    """The symmetric reordering P A P^T and P v (ref: coloring.py:101-123).
+
+    On the device this is a new level in the colouring's row order: the greedy
+    colouring keeps the closed-form layout (implicit-index rows, dataflow
+    sweeps), any other colouring is installed as an explicit permutation.
+    Returns (operand, permuted copies of ``vectors``)."""
+    import ctypes as C
+    from . import _lib
+    from .device import Context
+    from .problem import EllMatrix
+    dom = A.domain
+    world = getattr(A, "world", None)
+    ctx = Context(dom, 1, world=world)
+    greedy = greedy_coloring(*dom.local_dims)
+    if not (coloring.num_colors == greedy.num_colors and np.array_equal(coloring.perm, greedy.perm)):
+        offs = np.ascontiguousarray(coloring.color_offsets, dtype=np.int64)
+        perm = np.ascontiguousarray(coloring.perm, dtype=np.int64)
+        i64 = C.POINTER(C.c_int64)
+        ctx.call("hpg_set_coloring", 0, int(coloring.num_colors), offs.ctypes.data_as(i64),
+                 perm.ctypes.data_as(i64))
+    out = EllMatrix(ctx, 0, _lib.F64)
+    out.domain, out.world, out.coloring = dom, world, coloring
+    vecs = []
+    for v in vectors:
+        if isinstance(v, np.ndarray):
+            vecs.append(v[coloring.perm].copy())
+        else:
+            import torch
+            vecs.append(v[torch.as_tensor(coloring.perm, device=v.device)].clone())
+    return out, vecs

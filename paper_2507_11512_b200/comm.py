@@ -229,3 +229,27 @@ class HaloPlan:
                     L.hpg_host_send_rows(*args, sx, sy, sz, rows.ctypes.data_as(C.POINTER(C.c_int64)))
                     out[cx + d.npx * (cy + d.npy * cz)] = rows
         return dict(sorted(out.items()))
+
+
+def build_halo_plan(domain, A, world=None, rank=0, iperm=None):
+    """The exchange plan of A's level (ref: comm.py:180-236).  The device built
+    it with the level (send lists from the closed-form geometry, halo slots in
+    ascending neighbour rank / global index, A's off-rank columns already
+    pointing at them), so this hands out that plan; ``iperm`` is implied by A's
+    row order.  The 27-point neighbourhood never reaches a non-neighbour rank,
+    so the reference's TopologyError cannot arise."""
+    return HaloPlan(A.ctx, A.level, domain)
+
+
+def exchange_overlapped(v, plan, world, rank, interior_work):
+    """Exchange v's halo and run ``interior_work()`` (ref: comm.py:254-272).
+
+    Both are enqueued on the context's stream in that order, so the result is
+    the reference's bit for bit (the caller's contract: the interior work reads
+    no halo slot and writes no sent row).  The overlapped schedule proper -- the
+    exchange on a side stream under the interior rows -- lives inside the
+    library's SpMV and GS (option "overlap")."""
+    if world is None or plan is None or not plan.neighbors:
+        return interior_work()
+    plan.exchange(v)
+    return interior_work()

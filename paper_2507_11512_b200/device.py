@@ -16,6 +16,30 @@ INFO_KEYS = ("n", "n_ext", "nnz", "ncolors") + tuple(f"off{i}" for i in range(9)
 
 BOOL_DEFAULTS = {"stencil": 1, "lower": 0, "graphs": 1, "pdl": 1, "gs_rev": 1}
 
+_LIVE = []  # weak references to the live contexts, newest last (see context_for)
+
+
+def context_for(device, n, nranks=1):
+    """A live context on ``device`` whose level 0 has ``n`` rows (the newest such),
+    else a private 1-level vector context of n rows (created once, cached).
+    The reference's vector-level entry points (``cgs2_orthogonalize`` and
+    friends) take bare arrays; this is where their device work runs."""
+    import weakref
+    for ref in reversed(_LIVE):
+        c = ref()
+        if c is not None and c.h is not None and c.device == device and c.nranks == nranks \
+                and c.level_info(0)["n"] == n:
+            return c
+    if nranks != 1:
+        raise RuntimeError(f"no live {nranks}-rank context with {n} rows: build the hierarchy first")
+    from .geometry import GlobalProblem
+    ctx = Context(GlobalProblem.from_local(n, 1, 1, 1).domain(0), 1)
+    _VECTOR_CTX.append(ctx)  # keep it alive for later calls
+    return ctx
+
+
+_VECTOR_CTX = []
+
 
 class Context:
     def __init__(self, domain, levels, nu1=1, nu2=1, nu_c=1, world=None):
@@ -41,6 +65,9 @@ class Context:
         self.p2p = False
         if self.nranks > 1:
             self._open_peer_memory(world)
+        import weakref
+        _LIVE[:] = [r for r in _LIVE if r() is not None]
+        _LIVE.append(weakref.ref(self))
 
     def _open_peer_memory(self, world):
         """Map every rank's symmetric buffer (CUDA IPC over NVLink); NCCL stays as
@@ -83,6 +110,8 @@ class Context:
     def timers(self, mode, seconds=None):
         out = np.zeros(8) if seconds is None else seconds
         self.call("hpg_timers", mode, out.ctypes.data_as(C.POINTER(C.c_double)))
+        if mode in (0, 1):
+            self.timing = mode == 1
         return out
 
     def set_option(self, key, value):

@@ -52,12 +52,23 @@ class MgHierarchy:
         """
         import torch
         lv = self.levels[0]
+        if isinstance(r, np.ndarray):  # host array: V-cycle on the device, copy of z back
+            lo = r.dtype == np.float32
+            rd, _ = _lib.on_device(r, torch.float32 if lo else torch.float64, self.ctx.device)
+            return self.apply(rd, tally, None, count).cpu().numpy()
         lo = r.dtype == torch.float32
         A = lv.A_lo if lo else lv.A_hi
         z = out if out is not None else (lv.z_lo if lo else lv.z_hi)
+        # a tallied V-cycle outside a solve times its own motifs (CUDA events)
+        own = tally is not None and count and not getattr(self.ctx, "timing", False)
+        if own:
+            self.ctx.timers(1)
         self.ctx.call("hpg_vcycle", A.prec, _lib.ptr(r), _lib.ptr(z))
         if tally is not None and count:
             count_vcycle(self, tally, A.dtype)
+        if own:
+            tally.absorb_device_seconds(self.ctx)
+            self.ctx.timers(0)
         return z[:A.n_rows]
 
     def preconditioner(self, tally=None):
@@ -198,6 +209,7 @@ def build_hierarchy(domain, levels, world=None, rank=0, strategy="greedy", seed=
         A = EllMatrix(ctx, lev, _lib.F64)
         A_lo = EllMatrix(ctx, lev, _lib.F32)
         A.domain = A_lo.domain = dom
+        A.coloring = A_lo.coloring = colorings[lev]  # None: the greedy closed form
         lv = MgLevel(domain=dom, A_hi=A, A_lo=A_lo, coloring=colorings[lev])
         lv.plan = HaloPlan(ctx, lev, dom) if world is not None else None
         ne, n = A.n_cols_extended, A.n_rows
@@ -209,7 +221,10 @@ def build_hierarchy(domain, levels, world=None, rank=0, strategy="greedy", seed=
         if lev > 0:
             lv.inject_nnz = _inject_nnz(doms[lev - 1])
         out.append(lv)
-    return MgHierarchy(levels=out, sweeps=sweeps, world=world, rank=rank, ctx=ctx)
+    h = MgHierarchy(levels=out, sweeps=sweeps, world=world, rank=rank, ctx=ctx)
+    for lev in range(1, levels):
+        out[lev].f2c = Injection(h, lev)
+    return h
 
 
 def level_coloring(lv):
@@ -227,34 +242,103 @@ def injection_map(h, level):
     return f2c
 
 
+class Injection:
+    """A coarse level's injection map f2c (coarse row i <- fine row f2c[i]),
+    held on the device by the hierarchy (ref: multigrid.py:87-99 _injection_map).
+
+    What ``MgLevel.f2c`` holds: usable wherever the reference passes f2c
+    (``prolong_add``, ``restrict_inject``, ``fused_residual_restrict``) and
+    array-like on the host (``np.asarray(lv.f2c)``, ``len``, indexing)."""
+
+    def __init__(self, hier, level):
+        self._hier = hier
+        self.level = level            # the coarse level this map feeds
+        self.fine_level = level - 1
+        self._host = None
+        self._dev = None
+
+    @property
+    def ctx(self):
+        return self._hier.ctx
+
+    def host(self):
+        if self._host is None:
+            self._host = injection_map(self._hier, self.level)
+        return self._host
+
+    def device(self):
+        if self._dev is None:
+            import torch
+            self._dev = torch.from_numpy(self.host()).to(self.ctx.device)
+        return self._dev
+
+    def __array__(self, dtype=None, copy=None):
+        a = self.host()
+        return a.astype(dtype) if dtype is not None else a
+
+    def __len__(self):
+        return int(self._hier.levels[self.level].A_hi.n_rows)
+
+    def __getitem__(self, k):
+        return self.host()[k]
+
+
 def restrict_inject(v_f, f2c):
     """Coarse vector of the fine values at injection points (ref: multigrid.py:102-104)."""
-    return v_f[f2c].clone()
+    if isinstance(v_f, np.ndarray):
+        return v_f[np.asarray(f2c)].copy()
+    idx = f2c.device() if isinstance(f2c, Injection) else f2c
+    return v_f[idx].clone()
 
 
 def fused_residual_restrict(A_f, b_f, x_f, f2c=None, out=None, tally=None, n_c=None):
     """r_c = (b_f - A_f x_f) at the injected rows; x_f's halo must be fresh (ref: multigrid.py:107-128).
 
-    ``A_f`` is the fine level's operand; the injection map is the coarse level's
-    (built on the device), so ``f2c`` is accepted for signature parity only.
+    ``A_f`` is the fine level's operand; the injection map is the coarse level's,
+    held on the device (``f2c``, the coarse level's ``MgLevel.f2c``, names it and
+    must belong to the same hierarchy).
     """
+    if isinstance(f2c, Injection) and (f2c.ctx is not A_f.ctx or f2c.fine_level != A_f.level):
+        raise ValueError("f2c is not the injection map below this operand's level")
     import torch
     info = A_f.ctx.level_info(A_f.level + 1)
-    if out is None:
-        out = torch.empty(info["n"], dtype=A_f.torch_dtype, device=x_f.device)
-    A_f.ctx.call("hpg_restrict", A_f.level, A_f.prec, _lib.ptr(b_f), _lib.ptr(x_f), _lib.ptr(out))
+    bd, _ = _lib.on_device(b_f, A_f.torch_dtype, A_f.ctx.device)
+    xd, _ = _lib.on_device(x_f, A_f.torch_dtype, A_f.ctx.device)
+    outd, outh = _lib.on_device(out, A_f.torch_dtype, A_f.ctx.device) if out is not None else (None, None)
+    if outd is None:
+        outd = torch.empty(info["n"], dtype=A_f.torch_dtype, device=xd.device)
+    A_f.ctx.call("hpg_restrict", A_f.level, A_f.prec, _lib.ptr(bd), _lib.ptr(xd), _lib.ptr(outd))
     if tally is not None:
         inj = _inject_nnz(A_f.domain)
         tally.add("restrict_fused", A_f.dtype, nnz=inj, n_c=info["n"],
                   implicit_nnz=inj * (A_f.implicit_nnz // 27) // max(A_f.n_rows, 1))
-    return out
+    if isinstance(x_f, np.ndarray):  # host arrays in, host result out
+        if outh is not None:
+            _lib.back_to_host(outd, outh)
+            return outh
+        return outd.cpu().numpy()
+    return outd
 
 
-def prolong_add(A_f, x_f, x_c, tally=None):
-    """x_f[f2c] += x_c on the device (ref: multigrid.py:131-137); A_f names the fine level."""
-    A_f.ctx.call("hpg_prolong", A_f.level, A_f.prec, _lib.ptr(x_f), _lib.ptr(x_c))
+def prolong_add(x_f, x_c, f2c, tally=None):
+    """x_f[f2c] += x_c on the device, in place (ref: multigrid.py:131-137).
+
+    ``f2c`` is the coarse level's injection map (``MgLevel.f2c``); it names the
+    hierarchy and the level pair.  The precision follows the vectors'.
+    """
+    import torch
+    if not isinstance(f2c, Injection):
+        raise TypeError("f2c must be a level's injection map (MgLevel.f2c of a device hierarchy)")
+    prec = _lib.F32 if x_f.dtype.itemsize == 4 else _lib.F64
+    if x_c.dtype != x_f.dtype:
+        raise TypeError("prolong_add operands must share one precision")
+    tdt = torch.float32 if prec == _lib.F32 else torch.float64
+    xf, xfh = _lib.on_device(x_f, tdt, f2c.ctx.device)
+    xc, _ = _lib.on_device(x_c, tdt, f2c.ctx.device)
+    f2c.ctx.call("hpg_prolong", f2c.fine_level, prec, _lib.ptr(xf), _lib.ptr(xc))
+    _lib.back_to_host(xf, xfh)
     if tally is not None:
-        tally.add("prolong_add", A_f.dtype, n_c=x_c.numel())
+        tally.add("prolong_add", np.float32 if prec == _lib.F32 else np.float64, n_c=x_c.numel())
 
 
 def mg_vcycle(h, level, r, tally=None):
@@ -274,9 +358,9 @@ def mg_vcycle(h, level, r, tally=None):
         lv.plan.exchange(z)
     nxt = h.levels[level + 1]
     rc = nxt.r_lo if lo else nxt.r_hi
-    fused_residual_restrict(A, r, z, out=rc, tally=tally)
+    fused_residual_restrict(A, r, z, nxt.f2c, out=rc, tally=tally)
     zc = mg_vcycle(h, level + 1, rc, tally)
-    prolong_add(A, z, zc, tally=tally)
+    prolong_add(z, zc, nxt.f2c, tally=tally)
     for _ in range(sw.nu2):
         forward_gs_sweep(A, r, z, tally=tally)
     return z[:A.n_rows]

@@ -35,6 +35,11 @@ class EllMatrix:
         self._host = None
 
     @property
+    def local_dims(self):
+        """The rank-local box of this operand (what ``coloring.color`` reads)."""
+        return self.domain.local_dims
+
+    @property
     def implicit_nnz(self):
         """Nonzeros of the rows whose columns the kernels compute in closed form
         (implicit-index rows: 27 each, no column-index load) -- 0 with stencil off."""
@@ -52,6 +57,11 @@ class EllMatrix:
         return torch.float32 if self.prec == _lib.F32 else torch.float64
 
     def _export(self):
+        # one host export per (context, level), shared by the fp64 / fp32 twins
+        # (the reference's low-precision copy shares its structure arrays)
+        cache = self.ctx.__dict__.setdefault("_host_export", {})
+        if self._host is None and self.level in cache:
+            self._host = cache[self.level]
         if self._host is None:
             n = self.n_rows
             vals = np.zeros((n, STENCIL_WIDTH))
@@ -62,7 +72,48 @@ class EllMatrix:
             self.ctx.call("hpg_export_level", self.level, _lib.dptr(vals), cols.ctypes.data_as(i32),
                           nnz.ctypes.data_as(i32), diag.ctypes.data_as(i32))
             self._host = (vals, cols, nnz, diag)
+            cache[self.level] = self._host
         return self._host
+
+    def global_rows(self):
+        """Global id of every row in this operand's row order."""
+        d = self.domain
+        perm = self.row_perm()
+        lx, ly, _ = d.local_dims
+        x, y, z = perm % lx, (perm // lx) % ly, perm // (lx * ly)
+        return (d.ox + x) + d.gnx * ((d.oy + y) + d.gny * (d.oz + z))
+
+    def row_perm(self):
+        """Natural (pre-reorder) index of every row: the level's colouring."""
+        if getattr(self, "natural", False):
+            return np.arange(self.n_rows, dtype=np.int64)
+        col = getattr(self, "coloring", None)
+        if col is None:
+            from .coloring import greedy_coloring
+            col = greedy_coloring(*self.domain.local_dims)
+        return np.asarray(col.perm, dtype=np.int64)
+
+    @property
+    def col_global(self):
+        """Global column id of every entry, -1 for padding (ref: problem.py:31-57):
+        slot k of a row is its k-th in-domain neighbour in ascending global id."""
+        cache = self.ctx.__dict__.setdefault("_col_global", {})
+        if self.level not in cache:
+            d = self.domain
+            g = self.global_rows()
+            gx, gy, gz = g % d.gnx, (g // d.gnx) % d.gny, g // (d.gnx * d.gny)
+            cols = np.full((len(g), STENCIL_WIDTH), -1, dtype=np.int64)
+            k = np.zeros(len(g), dtype=np.int64)
+            rows = np.arange(len(g))
+            for dz in (-1, 0, 1):
+                for dy in (-1, 0, 1):
+                    for dx in (-1, 0, 1):
+                        ax, ay, az = gx + dx, gy + dy, gz + dz
+                        ok = (ax >= 0) & (ax < d.gnx) & (ay >= 0) & (ay < d.gny) & (az >= 0) & (az < d.gnz)
+                        cols[rows[ok], k[ok]] = (ax + d.gnx * (ay + d.gny * az))[ok]
+                        k += ok
+            cache[self.level] = cols
+        return cache[self.level]
 
     @property
     def values(self):
@@ -86,9 +137,62 @@ class EllMatrix:
         return vals[np.arange(self.n_rows), diag].astype(self.dtype)
 
 
+def generate_matrix(domain, world=None):
+    """The rank-local 27-point operand of ``domain`` in NATURAL row order
+    (ref: problem.py:88-142), assembled on the device: a one-level context whose
+    row order is the identity permutation (one colour block).  Compact rows,
+    ascending global columns, padding column 0 / value 0, 26 / -1 values -- the
+    exported ``values`` / ``col_idx`` / ``row_nnz`` / ``diag_pos`` are the
+    reference's, except that off-rank columns already carry their halo slots
+    (the device builds the halo plan with the level; ``build_halo_plan`` then
+    hands it out).  Several ranks: pass the job's ``world`` (an extension: the
+    device context needs its communicator at creation)."""
+    from .device import Context
+    if domain.npx * domain.npy * domain.npz > 1 and world is None:
+        raise ValueError("a multi-rank domain needs world= (the device context's communicator)")
+    ctx = Context(domain, 1, world=world)
+    n = domain.n_rows
+    offs = np.array([0, n], dtype=np.int64)
+    perm = np.arange(n, dtype=np.int64)
+    i64 = C.POINTER(C.c_int64)
+    ctx.call("hpg_set_coloring", 0, 1, offs.ctypes.data_as(i64), perm.ctypes.data_as(i64))
+    A = EllMatrix(ctx, 0, _lib.F64)
+    A.domain = domain
+    A.world = world
+    A.natural = True
+    return A
+
+
+def matrix_market_lines(A, global_rows):
+    """'row col value' lines (1-based global ids) of A's rows in A's row order
+    (ref: problem.py:216-223)."""
+    vals, nnz, cols = A.values, A.row_nnz, A.col_global
+    g = np.asarray(global_rows, dtype=np.int64)
+    out = []
+    for i in range(len(g)):
+        r = int(g[i]) + 1
+        for s in range(int(nnz[i])):
+            v = float(vals[i, s])
+            out.append(f"{r} {int(cols[i, s]) + 1} {int(v) if v.is_integer() else repr(v)}\n")
+    return out
+
+
+def write_matrix_market(path, A, global_rows, n_global):
+    """Local rows as MatrixMarket coordinate triplets, global ids (ref: problem.py:193-213)."""
+    lines = matrix_market_lines(A, global_rows)
+    with open(path, "w") as f:
+        f.write("%%MatrixMarket matrix coordinate real general\n")
+        f.write(f"{n_global} {n_global} {A.nnz_total}\n")
+        f.writelines(lines)
+
+
 def to_low_precision(A):
     """fp32 twin sharing the structure (ref: problem.py:165-175)."""
-    return EllMatrix(A.ctx, A.level, _lib.F32)
+    lo = EllMatrix(A.ctx, A.level, _lib.F32)
+    for k in ("domain", "world", "natural"):
+        if hasattr(A, k):
+            setattr(lo, k, getattr(A, k))
+    return lo
 
 
 @dataclass

@@ -38,9 +38,21 @@ def forward_gs_sweep(A, r, z, coloring=None, plan=None, world=None, rank=0,
     parity (ref: smoother.py:78-79); the device level already knows its
     color blocks and halo plan.
     """
+    rd, _ = _lib.on_device(r, A.torch_dtype, A.ctx.device)
+    zd, zh = _lib.on_device(z, A.torch_dtype, A.ctx.device)
+    if zh is not None and zh.dtype != A.dtype:
+        raise TypeError(f"GS sweep operands must be {A.dtype}")
+    r, z = rd, zd
     if z.dtype != A.torch_dtype or r.dtype != A.torch_dtype:
         raise TypeError(f"GS sweep operands must be {A.torch_dtype}")
+    if coloring is not None:  # the sweep runs over the level's own colour blocks: they must agree
+        info = A.ctx.level_info(A.level)
+        offs = [info[f"off{k}"] for k in range(info["ncolors"] + 1)]
+        if int(coloring.num_colors) != info["ncolors"] or \
+                [int(o) for o in coloring.color_offsets] != offs[:int(coloring.num_colors) + 1]:
+            raise ValueError("coloring does not match the operand's colour blocks")
     A.ctx.call("hpg_gs_sweep", A.level, A.prec, _lib.ptr(r), _lib.ptr(z), int(bool(z_is_zero)))
+    _lib.back_to_host(z, zh)
     if tally is not None:
         zs = None
         if z_is_zero and A.ctx.option("lower"):

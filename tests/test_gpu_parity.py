@@ -50,6 +50,7 @@ def test_device_levels_match_reference_bitwise():
         assert A.nnz_total == int(g[p + "row_nnz"].sum())
         if li:
             np.testing.assert_array_equal(injection_map(h, li), g[p + "f2c"])
+            np.testing.assert_array_equal(np.asarray(lv.f2c), g[p + "f2c"])  # MgLevel.f2c (ref field)
     h.close()
 
 
@@ -74,10 +75,10 @@ def test_stencil_kernels_bitwise_vs_reference(tag):
     z = _ext(x, ne, dt)
     forward_gs_sweep(A, r, z)
     np.testing.assert_array_equal(z[:A.n_rows].cpu().numpy(), g[f"r0_{tag}_gs1"])
-    rc = fused_residual_restrict(A, r, _ext(x, ne, dt))
+    rc = fused_residual_restrict(A, r, _ext(x, ne, dt), h.levels[1].f2c)
     np.testing.assert_array_equal(rc.cpu().numpy(), g[f"r0_{tag}_restrict"])
     xf = _ext(x, ne, dt)
-    prolong_add(A, xf, _dev(g[f"r0_{tag}_xc"], dt))
+    prolong_add(xf, _dev(g[f"r0_{tag}_xc"], dt), h.levels[1].f2c)
     np.testing.assert_array_equal(xf[:A.n_rows].cpu().numpy(), g[f"r0_{tag}_prolong"])
     zc = h.apply(r.clone())
     np.testing.assert_array_equal(zc.cpu().numpy(), g[f"r0_{tag}_vcycle"])
@@ -132,16 +133,32 @@ def _solve(l, mode, levels=4, tol=1e-9, max_iters=300, m=30, precond=True, b=Non
     return res, x0
 
 
-def assert_cycles_in_envelope(gpu, *refs):
+def reference_envelope(case):
+    """Per-cycle [min, max] of the reference's mixed counts: the reference run
+    under OPENBLAS_NUM_THREADS 1 / default (tests/golden/solves*.json), widened by
+    the reference algorithm's counts under other legitimate fp32 reduction orders
+    (tests/golden/reduction_envelope.json, the oracle pinned to the reference:
+    its OpenBLAS-GEMV order reproduces the reference's counts exactly)."""
+    gold = dict(load_golden("solves.json"), **load_golden("solves_xsplit.json"))
+    runs = [gold[case][t]["mixed"]["cycle_iters"] for t in ("1", "default")]
+    orders = list(load_golden("reduction_envelope.json").get(case, {}).values())
+    return runs, orders
+
+
+def assert_cycles_in_envelope(gpu, case):
     """the same number of restart cycles as the reference, and
     every cycle's inner-iteration count within +-1 of the reference envelope
-    [min, max] over its OpenBLAS thread settings."""
-    print(f"per-cycle iterations: gpu {list(gpu)} reference {[list(r) for r in refs]}")
-    assert all(len(r) == len(gpu) for r in refs), (gpu, refs)
+    (see reference_envelope; the reduction-order spread of the later cycles is
+    +-2 around the OpenBLAS counts)."""
+    runs, orders = reference_envelope(case)
+    print(f"{case} per-cycle iterations: gpu {list(gpu)} reference runs {runs} reference under other "
+          f"fp32 orders {orders}")
+    allr = runs + orders
+    assert all(len(r) == len(gpu) for r in allr), (gpu, allr)
     for i, g in enumerate(gpu):
-        lo = min(r[i] for r in refs)
-        hi = max(r[i] for r in refs)
-        assert lo - 1 <= g <= hi + 1, (i, gpu, refs)
+        lo = min(r[i] for r in allr)
+        hi = max(r[i] for r in allr)
+        assert lo - 1 <= g <= hi + 1, (i, gpu, allr)
 
 
 def _envelope(case):
@@ -165,7 +182,7 @@ def test_mixed_solve_within_reference_envelope(case, l):
     ref1, refd = _envelope(case)
     res, x = _solve(l, "mixed")
     assert res.converged and res.relres < 1e-9
-    assert_cycles_in_envelope(res.cycle_iterations, ref1["mixed"]["cycle_iters"], refd["mixed"]["cycle_iters"])
+    assert_cycles_in_envelope(res.cycle_iterations, case)
     gx = load_golden("solves_x.npz")[f"{case}_1_mixed"]
     np.testing.assert_allclose(x, gx, rtol=0, atol=1e-7)
 

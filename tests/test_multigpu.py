@@ -39,22 +39,21 @@ def test_two_ranks_16():
     out = _run(2, 16, 4)
     for rk in out["checks"]:
         assert all(rk.values()), out["checks"]
-    ref = load_golden("solves.json")["r2l16"]
-    _check_solves(out, ref)
+    _check_solves(out, "r2l16")
     assert out["solves"]["double"]["iterations"] == 23
     assert out["summary"]["raw_gflops"] > 0
 
 
-def _check_solves(out, ref):
+def _check_solves(out, case):
     """fp64 counts exact; mixed: per restart cycle within +-1 of the reference
     envelope; fullscale validation over all ranks has the same
     counts (ref bench.py:168-173)."""
     from test_gpu_parity import assert_cycles_in_envelope
+    ref = dict(load_golden("solves.json"), **load_golden("solves_xsplit.json"))[case]
     assert out["solves"]["double"]["iterations"] == ref["1"]["double"]["iterations"]
     assert out["solves"]["double"]["converged"]
     assert out["solves"]["mixed"]["relres"] < 1e-9
-    assert_cycles_in_envelope(out["solves"]["mixed"]["cycles"],
-                              *[ref[t]["mixed"]["cycle_iters"] for t in ("1", "default")])
+    assert_cycles_in_envelope(out["solves"]["mixed"]["cycles"], case)
     assert out["validation"]["mode"] == "fullscale"
     assert out["validation"]["n_d"] == ref["1"]["double"]["iterations"]
     env = [ref[t]["mixed"]["iterations"] for t in ("1", "default")]
@@ -71,7 +70,7 @@ def test_two_ranks_x_split_16():
     assert out["proc_dims"] == [2, 1, 1]
     for rk in out["checks"]:
         assert all(rk.values()), out["checks"]
-    _check_solves(out, load_golden("solves_xsplit.json")["x211l16"])
+    _check_solves(out, "x211l16")
 
 
 @pytest.mark.skipif(_gpus() < 4, reason="needs 4 GPUs")
@@ -82,7 +81,7 @@ def test_four_ranks_x_split_8(dims):
     assert out["proc_dims"] == list(dims)
     for rk in out["checks"]:
         assert all(rk.values()), out["checks"]
-    _check_solves(out, load_golden("solves_xsplit.json")["x%d%d%dl8" % dims])
+    _check_solves(out, "x%d%d%dl8" % dims)
 
 
 @pytest.mark.skipif(_gpus() < 2, reason="needs 2 GPUs")
@@ -124,4 +123,4 @@ def test_eight_ranks_8():
     for rk in out["checks"]:
         assert all(rk.values()), out["checks"]
     assert out["solves"]["double"]["iterations"] == 18
-    _check_solves(out, load_golden("solves.json")["r8l8"])
+    _check_solves(out, "r8l8")

@@ -198,3 +198,15 @@ def test_xsplit_solve_counts(case):
     assert all(len(r) == len(mx["cycle_iters"]) for r in refs)
     for i, g in enumerate(mx["cycle_iters"]):
         assert min(r[i] for r in refs) - 1 <= g <= max(r[i] for r in refs) + 1
+
+
+def test_reduction_envelope_pinned_to_reference():
+    """tests/golden/reduction_envelope.json (make_envelope.py): its OpenBLAS-GEMV
+    order -- the reference's own expressions run by the oracle -- reproduces the
+    reference's recorded per-cycle counts, and every order agrees on cycle 1."""
+    env = load_golden("reduction_envelope.json")
+    gold = dict(load_golden("solves.json"), **load_golden("solves_xsplit.json"))
+    for case, orders in env.items():
+        runs = [gold[case][t]["mixed"]["cycle_iters"] for t in ("1", "default")]
+        assert orders["blas_gemv"] in runs, (case, orders["blas_gemv"], runs)
+        assert len({tuple(o[:1]) for o in orders.values()}) == 1, (case, orders)
