@@ -31,6 +31,18 @@ def main():
     hier.apply(torch.randn(n, device="cuda"))
     torch.cuda.synchronize()
     hier.close()
+    # the tensor-copy staged kernels (colour passes, brick passes, SpMV, residual)
+    # on every level that admits them, at 32^3
+    cfg = BenchConfig(local_nx=32, local_ny=32, local_nz=32, time_seconds=0)
+    hier, lv, b = _build_state(cfg, 1, None, 0)
+    for brick in (0, 3):
+        hier.ctx.set_option("tma_min_rows", 0)
+        hier.ctx.set_option("brick", brick)
+        for mode in ("mixed", "double"):
+            r = _solve(cfg, hier, lv, b, None, 0, mode, 1e-9, 40)
+            print("tma", brick, mode, r.iterations, r.relres)
+    torch.cuda.synchronize()
+    hier.close()
     print("sanitize run ok")
 
 
