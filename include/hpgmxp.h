@@ -97,6 +97,13 @@ int hpg_export_level(hpg_ctx* ctx, int level, double* values, int32_t* col_idx,
  * ELL, send lists and the injection maps touching it (general gather kernels
  * then serve restriction / prolongation).  Synchronises. */
 int hpg_set_coloring(hpg_ctx* ctx, int level, int ncolors, const int64_t* offsets, const int64_t* perm);
+/* Jones-Plassmann-Luby colouring of an lx x ly x lz box on device `device`
+ * (ref: coloring.py:56-70, color(A, "jpl", seed)): colors[n] receives each
+ * natural row's colour, bit-identical to the reference -- same random stream:
+ * state / inc are the low / high 64-bit words of numpy's PCG64 state and
+ * increment of default_rng(seed); *rounds the independent-set rounds taken. */
+int hpg_jpl_color(int device, int lx, int ly, int lz, const uint64_t* state, const uint64_t* inc, int32_t* colors,
+                  int* rounds);
 /* Injection map f2c of coarse level `level` (>=1) into its parent (ref: multigrid.py:87-99). */
 int hpg_export_f2c(hpg_ctx* ctx, int level, int64_t* f2c);
 

@@ -42,6 +42,7 @@ SIGNATURES = {
     "hpg_export_level": (_i, [_p, _i, _dp, _i32p, _i32p, _i32p]),
     "hpg_export_f2c": (_i, [_p, _i, _i64p]),
     "hpg_set_coloring": (_i, [_p, _i, _i, _i64p, _i64p]),
+    "hpg_jpl_color": (_i, [_i, _i, _i, _i, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), _i32p, _ip]),
     "hpg_spmv": (_i, [_p, _i, _i, _p, _p]),
     "hpg_exchange": (_i, [_p, _i, _i, _p]),
     "hpg_gs_sweep": (_i, [_p, _i, _i, _p, _p, _i]),

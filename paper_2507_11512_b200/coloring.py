@@ -64,6 +64,40 @@ def _local_neighbours(lx, ly, lz, rows):
     return out
 
 
+def jpl_coloring_device(lx, ly, lz, seed=0, device=None):
+    """JPL on the GPU (csrc/hpg_jpl.cuh, ``hpg_jpl_color``): the reference's
+    rounds with its exact random stream -- numpy's default_rng(seed) PCG64 state
+    handed to the device, each draw reached by jump-ahead.  Bit-identical to
+    ``jpl_coloring`` and the reference (ref: coloring.py:56-70)."""
+    import ctypes as C
+    from . import _lib
+    if device is None:
+        import torch
+        device = torch.cuda.current_device()
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    m64 = (1 << 64) - 1
+    state = (C.c_uint64 * 2)(st["state"] & m64, st["state"] >> 64)
+    inc = (C.c_uint64 * 2)(st["inc"] & m64, st["inc"] >> 64)
+    n = lx * ly * lz
+    colors = np.empty(n, dtype=np.int32)
+    rounds = C.c_int()
+    _lib.check(_lib.lib().hpg_jpl_color(int(device), lx, ly, lz, state, inc,
+                                        colors.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(rounds)))
+    return _coloring_from_colors(colors)
+
+
+def _coloring_from_colors(colors):
+    n = len(colors)
+    num_colors = int(colors.max()) + 1 if n else 0
+    counts = np.bincount(colors, minlength=num_colors)
+    offsets = np.zeros(num_colors + 1, dtype=np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    perm = np.argsort(colors, kind="stable").astype(np.int64)  # (colour, natural index)
+    iperm = np.empty_like(perm)
+    iperm[perm] = np.arange(n, dtype=np.int64)
+    return Coloring(color=colors, num_colors=num_colors, color_offsets=offsets, perm=perm, iperm=iperm)
+
+
 def jpl_coloring(lx, ly, lz, seed=0, chunk=1 << 20):
     """Jones-Plassmann-Luby coloring, vectorised, identical to the reference's
     (ref: coloring.py:56-70): each round draws rng.random(n); a remaining row is
@@ -116,6 +150,14 @@ def color(A_or_dims, strategy="greedy", seed=0):
     if strategy == "greedy":
         return greedy_coloring(*dims)
     if strategy == "jpl":
+        # on the GPU when there is one (setup at 256^3 in well under a second); the
+        # vectorised host restatement otherwise (CPU-only tooling and tests)
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return jpl_coloring_device(*dims, seed=seed)
+        except ImportError:
+            pass
         return jpl_coloring(*dims, seed=seed)
     raise ValueError(f"unknown coloring strategy: {strategy!r}")
 

@@ -24,6 +24,7 @@
 #include "hpg_lower.cuh"
 #include "hpg_tma.cuh"
 #include "hpg_brick.cuh"
+#include "hpg_jpl.cuh"
 
 using hpg::Geom;
 
@@ -2360,3 +2361,62 @@ int hpg_timers(hpg_ctx* c, int mode, double* seconds) {
 }
 
 }  // extern "C"
+
+
+// Jones-Plassmann-Luby colouring of an lx x ly x lz box on the device, bit-identical to
+// the reference's numpy loop (ref: coloring.py:56-70; csrc/hpg_jpl.cuh).  state / inc:
+// numpy's PCG64 state (low, high 64-bit words) of default_rng(seed).
+int hpg_jpl_color(int device, int lx, int ly, int lz, const uint64_t* state, const uint64_t* inc, int32_t* colors,
+                  int* rounds) {
+  if (lx < 0 || ly < 0 || lz < 0 || !state || !inc || !colors) return fail(HPG_E_ARG, "bad JPL arguments");
+  const int64_t n = (int64_t)lx * ly * lz;
+  if (rounds) *rounds = 0;
+  if (n == 0) return HPG_OK;
+  CUDA_TRY(cudaSetDevice(device));
+  cudaStream_t st;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  double* w = nullptr;
+  int32_t* col = nullptr;
+  uint8_t* sel = nullptr;
+  unsigned long long* cnt = nullptr;
+  int rc = HPG_OK;
+  if (cudaMalloc(&w, n * 8) != cudaSuccess || cudaMalloc(&col, n * 4) != cudaSuccess ||
+      cudaMalloc(&sel, n) != cudaSuccess || cudaMalloc(&cnt, 8) != cudaSuccess) {
+    rc = fail(HPG_E_CUDA, "JPL buffers");
+  }
+  hpg::U128 base{state[0], state[1]};
+  const hpg::U128 inc128{inc[0], inc[1]};
+  int64_t colored = 0;
+  int r = 0;
+  if (!rc && cudaMemsetAsync(col, 0xff, n * 4, st) != cudaSuccess) rc = fail(HPG_E_CUDA, "JPL memset");
+  while (!rc && colored < n) {
+    const int grid = (int)cdiv(n, 256);
+    hpg::k_jpl_weights<<<grid, 256, 0, st>>>(n, base, inc128, w);
+    hpg::k_jpl_select<<<grid, 256, 0, st>>>(lx, ly, lz, w, col, sel);
+    cudaMemsetAsync(cnt, 0, 8, st);
+    hpg::k_jpl_color<<<grid, 256, 0, st>>>(lx, ly, lz, sel, col, cnt);
+    unsigned long long got = 0;
+    if (cudaMemcpyAsync(&got, cnt, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      rc = fail(HPG_E_CUDA, "JPL round: %s", cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    if (got == 0) {
+      rc = fail(HPG_E_CUDA, "JPL made no progress");
+      break;
+    }
+    colored += (int64_t)got;
+    base = hpg::pcg_advance(base, inc128, (uint64_t)n);  // the next round's rng.random(n)
+    ++r;
+  }
+  if (!rc && (cudaMemcpyAsync(colors, col, n * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+              cudaStreamSynchronize(st) != cudaSuccess))
+    rc = fail(HPG_E_CUDA, "JPL copy-out");
+  cudaFree(w);
+  cudaFree(col);
+  cudaFree(sel);
+  cudaFree(cnt);
+  cudaStreamDestroy(st);
+  if (rounds) *rounds = r;
+  return rc;
+}

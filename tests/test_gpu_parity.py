@@ -340,6 +340,42 @@ def test_cgs2_and_gemv_combine_vs_fp64_oracle(dt, kb):
     h.close()
 
 
+@pytest.mark.parametrize("key", ["4x4x4_s0", "6x4x8_s3", "8x8x8_s11", "5x3x4_s7", "16x16x16_s0"])
+def test_jpl_on_device_bitwise_vs_reference(key):
+    """JPL on the GPU (hpg_jpl_color) against the reference's colourings
+    (tests/golden/jpl.npz, ref: coloring.py:56-70): same random stream, same
+    colours, permutation and offsets."""
+    from paper_2507_11512_b200.coloring import jpl_coloring_device
+    g = load_golden("jpl.npz")
+    dims, seed = key.split("_s")
+    c = jpl_coloring_device(*map(int, dims.split("x")), int(seed))
+    np.testing.assert_array_equal(c.color, g["color_" + key])
+    np.testing.assert_array_equal(c.perm, g["perm_" + key])
+    np.testing.assert_array_equal(c.color_offsets, g["offsets_" + key])
+
+
+def test_jpl_on_device_matches_host_and_scales():
+    """Device JPL == the host restatement (bit-identical to the reference) at 32^3
+    over several seeds, and a valid colouring at 256^3 (16.8 M rows) in seconds --
+    the host loop needs minutes there."""
+    import time
+    from paper_2507_11512_b200.coloring import _local_neighbours, jpl_coloring, jpl_coloring_device
+    for seed in (0, 1, 5):
+        d = jpl_coloring_device(32, 32, 32, seed)
+        h = jpl_coloring(32, 32, 32, seed)
+        np.testing.assert_array_equal(d.color, h.color)
+    t0 = time.perf_counter()
+    c = jpl_coloring_device(256, 256, 256, 0)
+    dt = time.perf_counter() - t0
+    print(f"device JPL 256^3: {dt:.2f} s, {c.num_colors} colours")
+    assert dt < 30 and c.num_colors <= 27
+    for a in range(0, 256 ** 3, 1 << 22):  # valid: no neighbour shares a colour
+        rows = np.arange(a, a + (1 << 22))
+        nb = _local_neighbours(256, 256, 256, rows)
+        cn = np.where(nb >= 0, c.color[np.where(nb >= 0, nb, 0)], -1)
+        assert not np.any(cn == c.color[rows][:, None])
+
+
 def test_jpl_hierarchy_and_vcycle_bitwise_vs_reference():
     """--coloring jpl (ref: coloring.py:56-70): device levels built from the host JPL
     permutation match the reference's arrays, and the V-cycle (general gather
