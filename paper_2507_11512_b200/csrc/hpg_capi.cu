@@ -277,7 +277,16 @@ struct hpg_ctx {
   // SpMV / fp64 residual with staged values: bit 0 fp64, bit 1 fp32; configurations
   int spmv_tma = 3;
   int spmv_cfg[2] = {3220, 6416};  // measured r02: fp32 SpMV 446 -> 417 us, fp64 683 -> 667 us
-  int resid_cfg = 6410;  // measured r02: residual 867 -> 800 us (32x20: 913)  // fp64 32x20: 762 us
+  int resid_cfg = 6410;
+  int restr_cfg[2] = {3220, 6416};  // fused residual + injection (MODE 2) [fp64, fp32]
+  int64_t l2_window = 0;   // > 0: persisting L2 set-aside (bytes) for z during the big colour passes
+  // face rows off rank interfaces compute their columns (hpg_tma.cuh st_face_cols) in:
+  // bit 0 SpMV / residual / restriction, bit 1 fp64 colour passes, bit 2 fp32 colour
+  // passes.  Measured r02 (256^3): SpMV fp32 424 -> 350 us, fp64 668 -> 580, residual
+  // 825 -> 752, fp64 sweep 761 -> 681; fp32 sweep 492 -> 508 (left on the index plane)
+  int face_cols = 3;
+  bool l2_limit_set = false;
+  size_t l2_setaside = 0, l2_maxwin = 0;  // measured r02: residual 867 -> 800 us (32x20: 913)  // fp64 32x20: 762 us
   unsigned* sweep_done = nullptr;  // pass counters of the persistent sweep
   std::vector<GraphEntry> gcache;
   uint64_t gclock = 0;
@@ -366,6 +375,36 @@ cudaError_t launch_pdl_smem(hpg_ctx* c, void (*k)(KArgs...), int grid, int block
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = c->pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...);
+}
+
+// launch_pdl_smem plus an L2 access-policy window (persisting hits on [base, base+bytes))
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_smem_win(hpg_ctx* c, const void* base, size_t bytes, float hit, void (*k)(KArgs...), int grid,
+                                int block, size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (c->pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (base && bytes) {
+    attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[na].val.accessPolicyWindow.base_ptr = (void*)base;
+    attr[na].val.accessPolicyWindow.num_bytes = bytes;
+    attr[na].val.accessPolicyWindow.hitRatio = hit;
+    attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...);
 }
 
@@ -672,9 +711,27 @@ int gs_pass_tma_t(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int
   if (p.st.on) {
     stencil_offsets(p.st, col, p.doff, &p.kmask);
     if (!zero) p.kmask = 0;
+    if (!(c->face_cols & (sizeof(T) == 4 ? 4 : 2))) p.st.ifc = 63;  // face rows read the index plane
   }
   if (p.nrows <= 0) return HPG_OK;
-  CUDA_TRY(launch_pdl_smem(c, hpg::k_gs_pass_tma<T, R, MB>, (int)cdiv(p.nrows, R), R, pass_smem<T, R>(), p, r, z));
+  if (c->l2_window > 0 && L.n >= c->tma_min_rows) {
+    // keep the smoothed vector resident in L2 across the colour passes: the
+    // other colours' z lines are re-read by every pass (option "l2_window")
+    if (!c->l2_limit_set) {
+      cudaDeviceProp prop;
+      CUDA_TRY(cudaGetDeviceProperties(&prop, c->device));
+      c->l2_setaside = std::min<size_t>((size_t)c->l2_window, (size_t)prop.persistingL2CacheMaxSize);
+      c->l2_maxwin = (size_t)prop.accessPolicyMaxWindowSize;
+      CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c->l2_setaside));
+      c->l2_limit_set = true;
+    }
+    const size_t bytes = std::min<size_t>((size_t)L.n * sizeof(T), c->l2_maxwin);
+    const float hit = std::min(1.0f, (float)c->l2_setaside / (float)bytes);
+    CUDA_TRY(launch_pdl_smem_win(c, (const void*)z, bytes, hit, hpg::k_gs_pass_tma<T, R, MB>, (int)cdiv(p.nrows, R), R,
+                                 pass_smem<T, R>(), p, r, z));
+  } else {
+    CUDA_TRY(launch_pdl_smem(c, hpg::k_gs_pass_tma<T, R, MB>, (int)cdiv(p.nrows, R), R, pass_smem<T, R>(), p, r, z));
+  }
   ++c->launches;
   return HPG_OK;
 }
@@ -694,7 +751,8 @@ int pass_rows(int code) { return code / 100; }
 
 // ---- brick colour pass (hpg_brick.cuh): values AND neighbour z staged by tensor copies
 #define HPG_SPMV_CFGS(X) X(float, 64, 16, 0) X(float, 128, 8, 0) X(float, 32, 32, 0) X(double, 32, 20, 0) \
-  X(double, 64, 10, 0) X(double, 64, 8, 0) X(double, 32, 20, 1) X(double, 64, 10, 1) X(double, 64, 8, 1)
+  X(double, 64, 10, 0) X(double, 64, 8, 0) X(double, 32, 20, 1) X(double, 64, 10, 1) X(double, 64, 8, 1) \
+  X(float, 64, 16, 2) X(float, 128, 8, 2) X(double, 32, 20, 2) X(double, 64, 10, 2)
 #define HPG_BRICK_CFGS(X) X(float, 256, 5) X(float, 256, 4) X(float, 128, 8) X(double, 128, 4) X(double, 128, 3) \
   X(double, 64, 8)
 
@@ -934,10 +992,20 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
 }
 
 template <typename T>
+bool spmv_tma_ok(hpg_ctx* c, const Level& L, int rows);
+template <typename T, int MODE>
+int spmv_tma(hpg_ctx* c, Level& L, const T* x, const T* b, T* y, double* partial, int64_t* nblocks,
+             const int32_t* dst = nullptr, int64_t rows = -1);
+
+template <typename T>
 int restrict_(hpg_ctx* c, int l, const T* rf, const T* zf, T* rcoarse) {
   Timed tm(c, M_RESTRICT);
   Level& F = c->lev[l];
   Level& C = c->lev[l + 1];
+  if (!C.f2c && spmv_tma_ok<T>(c, F, c->restr_cfg[sizeof(T) == 4] / 100)) {
+    // the fine colour-0 rows [0, C.n) with staged values; rc[inj[j]] = r[j] - (A z)[j]
+    return spmv_tma<T, 2>(c, F, zf, rf, rcoarse, nullptr, nullptr, (const int32_t*)C.inj, C.n);
+  }
   if (C.f2c)
     CUDA_TRY(launch_pdl(c, hpg::k_restrict_gen<T>, grid_for(C.n), 256, F.cols, (const T*)vals_of<T>(F), F.ld, C.n,
                         (const int32_t*)C.f2c, rf, zf, rcoarse));
@@ -1389,6 +1457,8 @@ int build_stencil(hpg_ctx* c, Level& L) {
   st.cx = st.n8 << st.bx;
   st.cy = st.n8 << st.by;
   st.cz = st.n8 << st.bz;
+  st.ifc = (g.ox > 0) | ((g.ox + g.lx < g.gx) << 1) | ((g.oy > 0) << 2) | ((g.oy + g.ly < g.gy) << 3) |
+           ((g.oz > 0) << 4) | ((g.oz + g.lz < g.gz) << 5);
   auto magic = [](uint64_t d) { return d == 1 ? uint64_t{0} : ~uint64_t{0} / d + 1; };  // ceil(2^64 / d); d = 1 special-cased
   st.mn8 = magic(st.n8);
   st.mhxy = magic(st.hxy);
@@ -1566,7 +1636,8 @@ int check_level(hpg_ctx* c, int l) {
 // ---- SpMV / residual with tensor-copy staged values (hpg_tma.cuh k_spmv_tma)
 
 template <typename T, int R, int MB, int MODE>
-int spmv_tma_t(hpg_ctx* c, Level& L, const T* x, const T* b, T* y, double* partial, int64_t* nblocks) {
+int spmv_tma_t(hpg_ctx* c, Level& L, const T* x, const T* b, T* y, double* partial, int64_t* nblocks,
+               const int32_t* dst = nullptr, int64_t rows = -1) {
   hpg::SpmvPlan p;
   memset(&p, 0, sizeof p);
   int rc0 = encode_value_map<T>(c, L, R, &p.vmap);
@@ -1579,26 +1650,29 @@ int spmv_tma_t(hpg_ctx* c, Level& L, const T* x, const T* b, T* y, double* parti
     p.n8 = p.st.n8;
     uint32_t km;
     for (int col = 0; col < 8; ++col) stencil_offsets(p.st, col, p.doff[col], &km);
+    if (!(c->face_cols & 1)) p.st.ifc = 63;  // face rows read the index plane
   } else {
     p.st.on = 0;
   }
-  const int ilv = std::max(1, c->spmv_ilv[sizeof(T) == 4]);
+  const int ilv = MODE == 2 ? 1 : std::max(1, c->spmv_ilv[sizeof(T) == 4]);
   p.ilv = ilv;
-  const int64_t nbk = cdiv(L.n, R);
+  if (rows >= 0) p.n = rows;  // MODE 2: the fine colour-0 rows
+  const int64_t nbk = cdiv(p.n, R);
   if (nblocks) *nblocks = nbk;
   const int grid = (int)(cdiv(nbk, ilv) * ilv);
   CUDA_TRY(launch_pdl_smem(c, hpg::k_spmv_tma<T, R, MB, MODE>, grid, R, (size_t)27 * R * sizeof(T) + 16, p, x, b, y,
-                           partial));
+                           partial, dst));
   ++c->launches;
   return HPG_OK;
 }
 
 template <typename T, int MODE>
-int spmv_tma(hpg_ctx* c, Level& L, const T* x, const T* b, T* y, double* partial, int64_t* nblocks) {
-  const int code = MODE == 1 ? c->resid_cfg : c->spmv_cfg[sizeof(T) == 4];
+int spmv_tma(hpg_ctx* c, Level& L, const T* x, const T* b, T* y, double* partial, int64_t* nblocks,
+             const int32_t* dst, int64_t rows) {
+  const int code = MODE == 1 ? c->resid_cfg : MODE == 2 ? c->restr_cfg[sizeof(T) == 4] : c->spmv_cfg[sizeof(T) == 4];
 #define HPG_SPMV_CASE(TT, R, MB, MD)                                                                  \
   if (std::is_same<T, TT>::value && MODE == MD && code == R * 100 + MB)                                \
-    return spmv_tma_t<TT, R, MB, MD>(c, L, (const TT*)x, (const TT*)b, (TT*)y, partial, nblocks);
+    return spmv_tma_t<TT, R, MB, MD>(c, L, (const TT*)x, (const TT*)b, (TT*)y, partial, nblocks, dst, rows);
   HPG_SPMV_CFGS(HPG_SPMV_CASE)
 #undef HPG_SPMV_CASE
   return fail(HPG_E_ARG, "unknown SpMV configuration %d", code);
@@ -1823,6 +1897,8 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     c->wave_blocks[1] = std::min(occ(wave_fn<float>(true)), occ(wave_fn<float>(false)));
     const char* tm = getenv("HPG_TMA");
     if (tm) c->tma = atoi(tm);
+    const char* fc = getenv("HPG_FACE_COLS");
+    if (fc) c->face_cols = atoi(fc);
     const char* tr = getenv("HPG_TMA_MIN_ROWS");
     if (tr) c->tma_min_rows = atoll(tr);
     if (tma_setup<float>(c, sms) || tma_setup<double>(c, sms)) return bail(HPG_E_CUDA);
@@ -2333,6 +2409,10 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   else if (!strcmp(key, "spmv_cfg64")) c->spmv_cfg[0] = (int)value;
   else if (!strcmp(key, "spmv_cfg32")) c->spmv_cfg[1] = (int)value;
   else if (!strcmp(key, "resid_cfg")) c->resid_cfg = (int)value;
+  else if (!strcmp(key, "restr_cfg64")) c->restr_cfg[0] = (int)value;
+  else if (!strcmp(key, "l2_window")) c->l2_window = value;
+  else if (!strcmp(key, "face_cols")) c->face_cols = (int)value;
+  else if (!strcmp(key, "restr_cfg32")) c->restr_cfg[1] = (int)value;
   else if (!strcmp(key, "brick_cfg64")) c->brick_cfg[0] = (int)value;
   else if (!strcmp(key, "brick_cfg32")) c->brick_cfg[1] = (int)value;
   else return fail(HPG_E_ARG, "unknown option %s", key);

@@ -152,6 +152,7 @@ struct Stencil {
   int lx, ly, lz;
   int bx, by, bz;            // parity bit of each axis in the color id
   uint64_t mn8, mhxy, mhx;   // ceil(2^64 / d): q = umul64hi(i, m) == i / d exactly for i, d < 2^32
+  int ifc;                   // bit 2a / 2a+1: the low / high face of axis a is a rank interface
 };
 
 #ifndef HPG_ST_MAGIC

@@ -166,6 +166,64 @@ __device__ __forceinline__ bool st_interior(const Stencil& st, int64_t i, int pc
   return x >= 1 && x <= st.lx - 2 && y >= 1 && y <= st.ly - 2 && z >= 1 && z <= st.lz - 2;
 }
 
+// Columns of a FACE row of colour pc in closed form (the row's compacted ELL
+// slots, ref: problem.py:127-138): slot k is the k-th in-box offset s of the
+// row's position class (table kFaceSlots), column i + doff[s] (the same
+// per-colour constants as the interior rows); slots past the row's nnz are
+// padding, column 0.  Rows whose
+// missing neighbours lie across a RANK INTERFACE (halo columns, numbered by the
+// halo plan) return false and read the index plane.  Replaces 27 sparse 4-byte
+// index loads per x-face row -- a 32-byte sector each.
+// k-th in-box offset (0..26, z-slowest) of a row whose position class per axis is
+// 0 (low face), 1 (interior) or 2 (high face); 27 = padding.  Built at compile time.
+struct FaceSlots {
+  unsigned char s[27][27];
+  constexpr FaceSlots() : s() {
+    for (int cls = 0; cls < 27; ++cls) {
+      const int cx = cls % 3, cy = (cls / 3) % 3, cz = cls / 9;
+      int k = 0;
+      for (int o = 0; o < 27; ++o) {
+        const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
+        const bool ok = !(cx == 0 && dx < 0) && !(cx == 2 && dx > 0) && !(cy == 0 && dy < 0) &&
+                        !(cy == 2 && dy > 0) && !(cz == 0 && dz < 0) && !(cz == 2 && dz > 0);
+        if (ok) s[cls][k++] = (unsigned char)o;
+      }
+      for (; k < 27; ++k) s[cls][k] = 27;
+    }
+  }
+};
+__constant__ FaceSlots kFaceSlots = FaceSlots();
+
+__device__ __forceinline__ bool st_face_cols(const Stencil& st, int64_t i, int pc, const int32_t* doff,
+                                             int32_t (&c)[27]) {
+  uint32_t pos = (uint32_t)(i - (int64_t)pc * st.n8);
+  const uint32_t Z = st_div(pos, st.hxy, st.mhxy);
+  pos -= Z * st.hxy;
+  const uint32_t Y = st_div(pos, st.hx, st.mhx);
+  const uint32_t X = pos - Y * st.hx;
+  const int x = (int)(2 * X + ((pc >> st.bx) & 1));
+  const int y = (int)(2 * Y + ((pc >> st.by) & 1));
+  const int z = (int)(2 * Z + ((pc >> st.bz) & 1));
+  const int cx = x == 0 ? 0 : (x == st.lx - 1 ? 2 : 1);
+  const int cy = y == 0 ? 0 : (y == st.ly - 1 ? 2 : 1);
+  const int cz = z == 0 ? 0 : (z == st.lz - 1 ? 2 : 1);
+  const int cut = (cx == 0 ? 1 : 0) | (cx == 2 ? 2 : 0) | (cy == 0 ? 4 : 0) | (cy == 2 ? 8 : 0) |
+                  (cz == 0 ? 16 : 0) | (cz == 2 ? 32 : 0);
+  if (cut & st.ifc) return false;
+  const unsigned char* tab = kFaceSlots.s[cz * 9 + cy * 3 + cx];
+#pragma unroll
+  for (int k = 0; k < 27; ++k) {
+    const int s = tab[k];
+    int32_t cc = 0;
+    if (s < 27) {
+      cc = (int32_t)i + doff[s];
+      if (s == 13) cc = ~cc;
+    }
+    c[k] = cc;
+  }
+  return true;
+}
+
 // z_i of one row of colour pc: values from the shared-memory tile sv (plane-major,
 // ROWS per plane), gathers through L1, the reference's slot-order arithmetic.
 template <typename T, int ROWS>
@@ -359,8 +417,10 @@ __global__ void __launch_bounds__(ROWS, MINB) k_gs_pass_tma(const __grid_constan
     }
   } else {
     int32_t c[27];
+    if (!(p.st.on && st_face_cols(p.st, i, p.color, p.doff, c))) {
 #pragma unroll
-    for (int s = 0; s < 27; ++s) c[s] = __ldg(p.cols + s * p.ld + i);
+      for (int s = 0; s < 27; ++s) c[s] = __ldg(p.cols + s * p.ld + i);
+    }
     T g[27];
 #pragma unroll
     for (int s = 0; s < 27; ++s) {
@@ -398,10 +458,13 @@ struct SpmvPlan {
   Stencil st;
 };
 
+// MODE 2: the fused residual + injection (ref: multigrid.py:107-128): rows are the
+// fine colour-0 rows [0, n), y[dst[i]] = b[i] - (A x)[i]
 template <typename T, int ROWS, int MINB, int MODE>
 __global__ void __launch_bounds__(ROWS, MINB) k_spmv_tma(const __grid_constant__ SpmvPlan p, const T* __restrict__ x,
                                                          const T* __restrict__ b, T* __restrict__ y,
-                                                         double* __restrict__ partial) {
+                                                         double* __restrict__ partial,
+                                                         const int32_t* __restrict__ dst = nullptr) {
   extern __shared__ __align__(128) unsigned char smem[];
   T* sv = (T*)smem;
   uint64_t* bar = (uint64_t*)(smem + (size_t)27 * ROWS * sizeof(T));
@@ -429,11 +492,13 @@ __global__ void __launch_bounds__(ROWS, MINB) k_spmv_tma(const __grid_constant__
 #pragma unroll
       for (int s = 0; s < 27; ++s) g[s] = xi[p.doff[col][s]];
     } else {
+      int32_t cf[27];
+      if (!(p.st.on && st_face_cols(p.st, i, col, p.doff[col], cf))) {
 #pragma unroll
-      for (int s = 0; s < 27; ++s) {
-        const int32_t cc = __ldg(p.cols + s * p.ld + i);
-        g[s] = x[cc < 0 ? ~cc : cc];
+        for (int s = 0; s < 27; ++s) cf[s] = __ldg(p.cols + s * p.ld + i);
       }
+#pragma unroll
+      for (int s = 0; s < 27; ++s) g[s] = x[cf[s] < 0 ? ~cf[s] : cf[s]];
     }
     mbar_wait(bar, 0);
     T acc = T(0);
@@ -441,6 +506,8 @@ __global__ void __launch_bounds__(ROWS, MINB) k_spmv_tma(const __grid_constant__
     for (int s = 0; s < 27; ++s) acc = add_rn(acc, mul_rn(sv[s * ROWS + t], g[s]));
     if (MODE == 0) {
       y[i] = acc;
+    } else if (MODE == 2) {
+      y[dst[i]] = sub_rn(b[i], acc);
     } else {
       const T rr = sub_rn(b[i], acc);
       y[i] = rr;
