@@ -282,9 +282,11 @@ struct hpg_ctx {
   int64_t l2_window = 0;   // > 0: persisting L2 set-aside (bytes) for z during the big colour passes
   // face rows off rank interfaces compute their columns (hpg_tma.cuh st_face_cols) in:
   // bit 0 SpMV / residual / restriction, bit 1 fp64 colour passes, bit 2 fp32 colour
-  // passes.  Measured r02 (256^3): SpMV fp32 424 -> 350 us, fp64 668 -> 580, residual
-  // 825 -> 752, fp64 sweep 761 -> 681; fp32 sweep 492 -> 508 (left on the index plane)
-  int face_cols = 3;
+  // passes; bit 3: colour passes take x-face rows through a compile-time slot map
+  // (st_xface).  Measured r02 (256^3): SpMV fp32 424 -> 350 us, fp64 668 -> 580,
+  // residual 825 -> 752, fp64 sweep 761 -> 681; fp32 sweep 489 -> 449 with bits 2+3
+  // (bit 2 alone: 513, bit 3 alone: 522)
+  int face_cols = 15;
   bool l2_limit_set = false;
   size_t l2_setaside = 0, l2_maxwin = 0;  // measured r02: residual 867 -> 800 us (32x20: 913)  // fp64 32x20: 762 us
   unsigned* sweep_done = nullptr;  // pass counters of the persistent sweep
@@ -711,7 +713,8 @@ int gs_pass_tma_t(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int
   if (p.st.on) {
     stencil_offsets(p.st, col, p.doff, &p.kmask);
     if (!zero) p.kmask = 0;
-    if (!(c->face_cols & (sizeof(T) == 4 ? 4 : 2))) p.st.ifc = 63;  // face rows read the index plane
+    p.xface = (c->face_cols & 8) ? 1 : 0;
+    if (!(c->face_cols & (sizeof(T) == 4 ? 4 : 2))) p.st.ifc = 63;  // other face rows read the index plane
   }
   if (p.nrows <= 0) return HPG_OK;
   if (c->l2_window > 0 && L.n >= c->tma_min_rows) {

@@ -224,6 +224,26 @@ __device__ __forceinline__ bool st_face_cols(const Stencil& st, int64_t i, int p
   return true;
 }
 
+// An x-face row (x == 0 or lx-1, y and z interior, the x face not a rank
+// interface): its 18 valid offsets are, per (dy, dz) pair in order, the two dx
+// on the box side -- slot k is offset 3 (k >> 1) + (k & 1) + (x == 0), a
+// compile-time map per side, so the columns cost no table lookups.  Returns
+// 0 (not such a row), 1 (low x face) or 2 (high x face).
+__device__ __forceinline__ int st_xface(const Stencil& st, int64_t i, int pc) {
+  uint32_t pos = (uint32_t)(i - (int64_t)pc * st.n8);
+  const uint32_t Z = st_div(pos, st.hxy, st.mhxy);
+  pos -= Z * st.hxy;
+  const uint32_t Y = st_div(pos, st.hx, st.mhx);
+  const uint32_t X = pos - Y * st.hx;
+  const int x = (int)(2 * X + ((pc >> st.bx) & 1));
+  const int y = (int)(2 * Y + ((pc >> st.by) & 1));
+  const int z = (int)(2 * Z + ((pc >> st.bz) & 1));
+  if (y < 1 || y > st.ly - 2 || z < 1 || z > st.lz - 2) return 0;
+  if (x == 0) return (st.ifc & 1) ? 0 : 1;
+  if (x == st.lx - 1) return (st.ifc & 2) ? 0 : 2;
+  return 0;
+}
+
 // z_i of one row of colour pc: values from the shared-memory tile sv (plane-major,
 // ROWS per plane), gathers through L1, the reference's slot-order arithmetic.
 template <typename T, int ROWS>
@@ -375,6 +395,7 @@ struct PassPlan {
   int color;
   uint32_t kmask;       // implicit-index rows: slot s's load skipped when bit s is set
   int32_t doff[27];     // implicit-index rows: slot s gathers column i + doff[s]
+  int xface;            // x-face rows use the compile-time slot map (st_xface)
   Stencil st;
 };
 
@@ -417,7 +438,20 @@ __global__ void __launch_bounds__(ROWS, MINB) k_gs_pass_tma(const __grid_constan
     }
   } else {
     int32_t c[27];
-    if (!(p.st.on && st_face_cols(p.st, i, p.color, p.doff, c))) {
+    const int xf = (p.st.on && p.xface) ? st_xface(p.st, i, p.color) : 0;
+    if (xf) {  // x-face row: compile-time slot map per side
+#pragma unroll
+      for (int k = 0; k < 27; ++k) {
+        int32_t cc = 0;
+        if (k < 18) {
+          const int s_lo = 3 * (k >> 1) + (k & 1) + 1, s_hi = 3 * (k >> 1) + (k & 1);
+          const int s = xf == 1 ? s_lo : s_hi;
+          cc = (int32_t)i + (xf == 1 ? p.doff[s_lo] : p.doff[s_hi]);
+          if (s == 13) cc = ~cc;
+        }
+        c[k] = cc;
+      }
+    } else if (!(p.st.on && st_face_cols(p.st, i, p.color, p.doff, c))) {
 #pragma unroll
       for (int s = 0; s < 27; ++s) c[s] = __ldg(p.cols + s * p.ld + i);
     }

@@ -17,6 +17,7 @@ def main():
     p.add_argument("--local", type=int, default=256)
     p.add_argument("--reps", type=int, default=20)
     p.add_argument("--opt", default="tma:0,3", help="option:valueA,valueB")
+    p.add_argument("--set", nargs="*", default=[], help="key=value options applied first")
     a = p.parse_args()
     import torch
     from paper_2507_11512_b200.bench import BenchConfig, _build_state
@@ -25,6 +26,9 @@ def main():
     hier, lv, b = _build_state(cfg, 1, None, 0)
     ctx = hier.ctx
     st = ctx.stream
+    for kv in a.set:
+        k, v = kv.split("=")
+        ctx.set_option(k, int(v))
     n, ne = lv.A_hi.n_rows, lv.A_hi.n_cols_extended
     key, vals = a.opt.split(":")
     vals = [int(v) for v in vals.split(",")]
