@@ -286,7 +286,7 @@ struct hpg_ctx {
   // (st_xface).  Measured r02 (256^3): SpMV fp32 424 -> 350 us, fp64 668 -> 580,
   // residual 825 -> 752, fp64 sweep 761 -> 681; fp32 sweep 489 -> 449 with bits 2+3
   // (bit 2 alone: 513, bit 3 alone: 522)
-  int face_cols = 15;
+  int face_cols = 31;  // bit 4: SpMV-type kernels take x-face rows through the slot map too (fp32 SpMV 349 -> 331 us)
   bool l2_limit_set = false;
   size_t l2_setaside = 0, l2_maxwin = 0;  // measured r02: residual 867 -> 800 us (32x20: 913)  // fp64 32x20: 762 us
   unsigned* sweep_done = nullptr;  // pass counters of the persistent sweep
@@ -1653,6 +1653,7 @@ int spmv_tma_t(hpg_ctx* c, Level& L, const T* x, const T* b, T* y, double* parti
     p.n8 = p.st.n8;
     uint32_t km;
     for (int col = 0; col < 8; ++col) stencil_offsets(p.st, col, p.doff[col], &km);
+    p.xface = (c->face_cols & 16) ? 1 : 0;
     if (!(c->face_cols & 1)) p.st.ifc = 63;  // face rows read the index plane
   } else {
     p.st.on = 0;

@@ -488,6 +488,7 @@ struct SpmvPlan {
   int64_t ld, n;
   int64_t n8;           // implicit-index rows: colour block size (a multiple of ROWS)
   int ilv;
+  int xface;            // x-face rows use the compile-time slot map (st_xface)
   int32_t doff[8][27];  // implicit-index rows of colour c: slot s reads column i + doff[c][s]
   Stencil st;
 };
@@ -527,7 +528,18 @@ __global__ void __launch_bounds__(ROWS, MINB) k_spmv_tma(const __grid_constant__
       for (int s = 0; s < 27; ++s) g[s] = xi[p.doff[col][s]];
     } else {
       int32_t cf[27];
-      if (!(p.st.on && st_face_cols(p.st, i, col, p.doff[col], cf))) {
+      const int xf = (p.st.on && p.xface) ? st_xface(p.st, i, col) : 0;
+      if (xf) {  // x-face row: compile-time slot map per side
+#pragma unroll
+        for (int k = 0; k < 27; ++k) {
+          int32_t cc = 0;
+          if (k < 18) {
+            const int s_lo = 3 * (k >> 1) + (k & 1) + 1, s_hi = 3 * (k >> 1) + (k & 1);
+            cc = (int32_t)i + (xf == 1 ? p.doff[col][s_lo] : p.doff[col][s_hi]);
+          }
+          cf[k] = cc;  // (no diagonal marker needed: the SpMV forms every product)
+        }
+      } else if (!(p.st.on && st_face_cols(p.st, i, col, p.doff[col], cf))) {
 #pragma unroll
         for (int s = 0; s < 27; ++s) cf[s] = __ldg(p.cols + s * p.ld + i);
       }

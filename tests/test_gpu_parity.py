@@ -479,7 +479,7 @@ def test_execution_variants_agree_bitwise():
                 assert with_tail < without, (with_tail, without)
         for key, val in variants:  # back to the defaults for the next round
             ctx.set_option(key, {"tail_rows": 0, "tail_cluster": 0, "gs_rev": 0, "pdl": 1, "known_zero": 1,
-                                 "wave": 3, "lower": 0, "tma": 3, "tma_min_rows": 1 << 18, "face_cols": 15}[key])
+                                 "wave": 3, "lower": 0, "tma": 3, "tma_min_rows": 1 << 18, "face_cols": 31}[key])
     ctx.set_option("graphs", 1)
     ctx.set_option("known_zero", 1)
     ctx.set_option("known_zero", 1)
