@@ -153,4 +153,187 @@ __global__ void __launch_bounds__(ROWS, MINB) k_gs_pass_brick(const __grid_const
   if (t == 0 && !interior) mbar_wait(bars + 1, 0);
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined brick pass (the default colour pass where the layout allows).
+//
+// k_gs_pass_brick exposes one round trip for its z boxes per CTA.  Here each
+// CTA is persistent over its share of the pass's bricks (round-robin, so the
+// grid works on one narrow window of the colour block at a time) with an
+// S-stage shared-memory ring: warp 0 (one lane) issues, per brick, the 2-D
+// tensor copy of the 27 value planes and the 4-D copies of the neighbour
+// colours' z boxes; the value copies of the first S bricks go out before the
+// PDL wait, everything else after it.  The ROWS consumer threads (one row
+// each) form their rows from shared memory alone and release the stage.  With
+// 3 CTAs x 3 stages per SM, nine bricks' operands are in flight per SM while
+// the consumers hold no gathered values in registers.
+// Face rows read their slots through the position-class table (kFaceSlots)
+// from the same boxes; rows whose missing neighbours are across a rank
+// interface (halo columns) take the indexed path with global gathers.
+// a row whose missing neighbours lie across a rank interface: indexed columns,
+// global gathers (the halo tail); out of line, so its 54 live registers do not
+// weigh on the shared-memory path
+template <typename T, int ROWS>
+__device__ __noinline__ T brick_interface_row(const BrickPlan& p, const T* sv, int t, int64_t i, const T* z, T ri) {
+  int32_t c[27];
+#pragma unroll
+  for (int s = 0; s < 27; ++s) c[s] = __ldg(p.cols + s * p.ld + i);
+  T g[27];
+#pragma unroll
+  for (int s = 0; s < 27; ++s) {
+    const int32_t cc = c[s] < 0 ? ~c[s] : c[s];
+    g[s] = (p.known0 >= 0 && cc >= p.known0) ? T(0) : z[cc];
+  }
+  T acc = T(0), d = T(0);
+#pragma unroll
+  for (int s = 0; s < 27; ++s) {
+    T vs = sv[s * ROWS + t];
+    if (c[s] < 0) {
+      d = vs;
+      vs = T(0);
+    }
+    acc = add_rn(acc, mul_rn(vs, g[s]));
+  }
+  return div_rn(sub_rn(ri, acc), d);
+}
+
+struct BrickPipe {
+  uint32_t stage_bytes;  // one ring stage: values, z boxes, r, own z (128-byte aligned parts)
+  uint32_t zoff;         // byte offset of the z boxes inside a stage
+  uint32_t roff;         // byte offset of the brick's r (ROWS values), then its own z
+  uint32_t vbytes;       // value bytes per brick
+  int64_t ntiles;        // bricks in this colour block
+};
+
+template <typename T, int ROWS, int S>
+__global__ void __launch_bounds__(32 + ROWS, 1) k_gs_brick_pp(const __grid_constant__ BrickPlan p,
+                                                              const __grid_constant__ BrickPipe q,
+                                                              const T* __restrict__ r, T* z) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = (uint64_t*)(smem + (size_t)S * q.stage_bytes);
+  uint64_t* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int64_t mine = q.ntiles > blockIdx.x ? (q.ntiles - blockIdx.x + G - 1) / G : 0;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < S; ++k) {
+      mbar_init(full + k, 1);
+      mbar_init(empty + k, ROWS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+  uint32_t zbytes = (uint32_t)(ROWS * sizeof(T)) * (p.known0 < 0 ? 2u : 1u);  // r (+ own z)
+#pragma unroll
+  for (int am = 1; am < 8; ++am)
+    if ((p.load_mask >> am) & 1u) zbytes += p.box_bytes[am];
+  auto tile_of = [&](int64_t m) {
+    const int64_t j = (int64_t)blockIdx.x + m * G;
+    return p.rev ? q.ntiles - 1 - j : j;
+  };
+  if (warp == 0) {  // ---- producer
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      auto issue_z = [&](int64_t m) {
+        const int64_t t0 = tile_of(m) * ROWS;
+        const int Z0 = (int)(t0 / p.hxy), Y0 = (int)((t0 - (int64_t)Z0 * p.hxy) / p.hx);
+        unsigned char* st = smem + (size_t)(m % S) * q.stage_bytes;
+        T* sz = (T*)(st + q.zoff);
+        // the brick's r and own z (contiguous rows) ride in the same stage
+        bulk_g2s(st + q.roff, r + p.row0 + t0, ROWS * sizeof(T), full + (m % S), pol);
+        if (p.known0 < 0) bulk_g2s(st + q.roff + ROWS * sizeof(T), z + p.row0 + t0, ROWS * sizeof(T), full + (m % S), pol);
+#pragma unroll
+        for (int am = 1; am < 8; ++am)
+          if ((p.load_mask >> am) & 1u)
+            tma_g2s_4d(sz + p.box_off[am], &p.zmap[am], p.box_x[am], Y0 + p.box_y[am], Z0 + p.box_z[am],
+                       p.box_c[am], full + (m % S));
+      };
+      const int64_t first = mine < S ? mine : S;
+      for (int64_t m = 0; m < first; ++m) {  // matrix planes ahead of the dependency
+        mbar_expect_tx(full + m, q.vbytes + zbytes);
+        tma_g2s_2d(smem + (size_t)m * q.stage_bytes, &p.vmap, (int)(p.row0 + tile_of(m) * ROWS), 0, full + m, pol);
+      }
+      pdl_wait();
+      for (int64_t m = 0; m < first; ++m) issue_z(m);
+      for (int64_t m = first; m < mine; ++m) {
+        const int k = (int)(m % S);
+        mbar_wait(empty + k, (uint32_t)(((m / S) - 1) & 1));
+        mbar_expect_tx(full + k, q.vbytes + zbytes);
+        tma_g2s_2d(smem + (size_t)k * q.stage_bytes, &p.vmap, (int)(p.row0 + tile_of(m) * ROWS), 0, full + k, pol);
+        issue_z(m);
+      }
+    }
+    return;
+  }
+  // ---- consumers: one row per thread per brick
+  const int t = threadIdx.x - 32;
+  pdl_wait();
+  const T z0 = (p.known0 >= 0 && p.known0 == 0) ? T(0) : z[0];  // padding slots gather column 0
+  const int rx = t % p.hx, ry = t / p.hx;
+  const int pc = p.color;
+  const int ta = t, tb = t + p.pad * ry;
+  for (int64_t m = 0; m < mine; ++m) {
+    const int k = (int)(m % S);
+    const int64_t t0 = tile_of(m) * ROWS;
+    const int64_t i = p.row0 + t0 + t;
+    const int Z0 = (int)(t0 / p.hxy), Y0 = (int)((t0 - (int64_t)Z0 * p.hxy) / p.hx);
+    const int x = 2 * rx + ((pc >> p.st.bx) & 1), y = 2 * (Y0 + ry) + ((pc >> p.st.by) & 1),
+              zc = 2 * Z0 + ((pc >> p.st.bz) & 1);
+    const int cx = x == 0 ? 0 : (x == p.st.lx - 1 ? 2 : 1);
+    const int cy = y == 0 ? 0 : (y == p.st.ly - 1 ? 2 : 1);
+    const int cz = zc == 0 ? 0 : (zc == p.st.lz - 1 ? 2 : 1);
+    const int cut = (cx == 0 ? 1 : 0) | (cx == 2 ? 2 : 0) | (cy == 0 ? 4 : 0) | (cy == 2 ? 8 : 0) |
+                    (cz == 0 ? 16 : 0) | (cz == 2 ? 32 : 0);
+    unsigned char* st = smem + (size_t)k * q.stage_bytes;
+    const T* sv = (const T*)st;
+    const T* sz = (const T*)(st + q.zoff);
+    mbar_wait(full + k, (uint32_t)((m / S) & 1));
+    const T ri = ((const T*)(st + q.roff))[t];
+    const T zi = p.known0 >= 0 ? T(0) : ((const T*)(st + q.roff))[ROWS + t];
+    T out;
+    if (cut & p.st.ifc) {
+      out = brick_interface_row<T, ROWS>(p, sv, t, i, z, ri);
+    } else {
+      T acc = T(0), d = T(0);
+      if (cut == 0) {  // interior: slot s is offset s
+#pragma unroll
+        for (int s = 0; s < 27; ++s) {
+          T vs = sv[s * ROWS + t];
+          T g;
+          if (s == 13) {
+            d = vs;
+            vs = T(0);
+            g = zi;
+          } else {
+            g = ((p.kmask >> s) & 1u) ? T(0) : sz[(((p.xsel >> s) & 1u) ? tb : ta) + p.sconst[s]];
+          }
+          acc = add_rn(acc, mul_rn(vs, g));
+        }
+      } else {  // a face row: slot k is the k-th in-box offset of its class
+        const unsigned char* tab = kFaceSlots.s[cz * 9 + cy * 3 + cx];
+#pragma unroll
+        for (int kk = 0; kk < 27; ++kk) {
+          const int s = tab[kk];
+          T vs = sv[kk * ROWS + t];
+          T g;
+          if (s == 27) {
+            g = z0;  // padding: value 0, column 0 (the reference's spmv_cols)
+          } else if (s == 13) {
+            d = vs;
+            vs = T(0);
+            g = zi;
+          } else {
+            g = ((p.kmask >> s) & 1u) ? T(0) : sz[(((p.xsel >> s) & 1u) ? tb : ta) + p.sconst[s]];
+          }
+          acc = add_rn(acc, mul_rn(vs, g));
+        }
+      }
+      out = div_rn(sub_rn(ri, acc), d);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + k);
+    z[i] = out;
+  }
+}
+
 }  // namespace hpg

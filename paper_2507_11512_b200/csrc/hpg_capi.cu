@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -274,6 +275,11 @@ struct hpg_ctx {
   int brick = 0;
   int brick_cfg[2] = {12804, 25605};
   size_t brick_smem_max = 64 * 1024;
+  // pipelined persistent brick pass: bit 0 fp64, bit 1 fp32; (rows * 10 + stages)
+  int bpp = 0;
+  int bpp_cfg[2] = {1282, 1283};
+  std::map<int, int> bpp_blocks;
+  std::map<int, size_t> bpp_smem;
   // SpMV / fp64 residual with staged values: bit 0 fp64, bit 1 fp32; configurations
   int spmv_tma = 3;
   int spmv_cfg[2] = {3220, 6416};  // measured r02: fp32 SpMV 446 -> 417 us, fp64 683 -> 667 us
@@ -775,18 +781,18 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder(hpg_ctx* c) {
 // the brick tiling applies: implicit-index layout, ROWS whole x-lines of one plane,
 // every box within the tensor-copy limits
 template <typename T>
-bool brick_ok(hpg_ctx* c, const Level& L, int rows) {
+bool brick_ok(hpg_ctx* c, const Level& L, int rows, bool any = false) {
   const hpg::Stencil st = stencil_of(c, L);
-  if (!st.on || !((c->brick >> (sizeof(T) == 4)) & 1)) return false;
+  if (!st.on || (!any && !((c->brick >> (sizeof(T) == 4)) & 1))) return false;
   const int pad = 16 / (int)sizeof(T);
   const int hx = (int)st.hx, hy = (int)st.hy;
   if (hx % pad || rows % hx || hy % (rows / hx) || hx + pad > 256 || rows / hx + 1 > 256) return false;
   return true;
 }
 
-template <typename T, int R, int MB>
-int gs_pass_brick_t(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int rev) {
-  hpg::BrickPlan p;
+// The brick plan of colour col (value map, z box maps and offsets, slot table)
+template <typename T>
+int brick_plan(hpg_ctx* c, Level& L, int col, T* z, int zero, int rev, int R, hpg::BrickPlan& p, int* zelems) {
   memset(&p, 0, sizeof p);
   int rc0 = encode_value_map<T>(c, L, R, &p.vmap);
   if (rc0) return rc0;
@@ -851,6 +857,17 @@ int gs_pass_brick_t(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, i
     if (am & 1) p.xsel |= 1u << s;
     if (zero && p.box_c[am] >= col) p.kmask |= 1u << s;
   }
+  *zelems = off;
+  return HPG_OK;
+}
+
+template <typename T, int R, int MB>
+int gs_pass_brick_t(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int rev) {
+  hpg::BrickPlan p;
+  int off = 0;
+  int rc0 = brick_plan<T>(c, L, col, z, zero, rev, R, p, &off);
+  if (rc0) return rc0;
+  const int w = (int)sizeof(T);
   if (p.nrows <= 0) return HPG_OK;
   const size_t zoff = (hpg::BrickSmem<T, R>::kValBytes + 127) / 128 * 128;
   const size_t smem = zoff + (size_t)off * w + 16;
@@ -869,6 +886,55 @@ int gs_pass_brick(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int
   HPG_BRICK_CFGS(HPG_BRICK_CASE)
 #undef HPG_BRICK_CASE
   return fail(HPG_E_ARG, "unknown brick-pass configuration %d", code);
+}
+
+// pipelined persistent brick pass (hpg_brick.cuh k_gs_brick_pp): (rows, stages)
+#define HPG_BPP_CFGS(X) X(float, 128, 3) X(float, 128, 2) X(float, 256, 2) X(double, 128, 2) X(double, 64, 3)
+
+template <typename T, int R, int S>
+int gs_pass_bpp_t(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int rev) {
+  hpg::BrickPlan p;
+  int zel = 0;
+  int rc0 = brick_plan<T>(c, L, col, z, zero, rev, R, p, &zel);
+  if (rc0) return rc0;
+  if (getenv("HPG_BPP_NOZ")) p.load_mask = 0;  // timing experiment only (wrong results)
+  hpg::BrickPipe q;
+  q.vbytes = (uint32_t)(27 * R * sizeof(T));
+  q.zoff = (q.vbytes + 127) / 128 * 128;
+  q.roff = (uint32_t)((q.zoff + (size_t)zel * sizeof(T) + 127) / 128 * 128);
+  q.stage_bytes = (uint32_t)((q.roff + 2 * R * sizeof(T) + 127) / 128 * 128);
+  q.ntiles = p.nrows / R;
+  if (p.nrows <= 0) return HPG_OK;
+  const size_t smem = (size_t)S * q.stage_bytes + 2 * S * 8;
+  auto fn = hpg::k_gs_brick_pp<T, R, S>;
+  const int key = (sizeof(T) == 4 ? 1000000 : 0) + R * 10 + S;
+  int& blocks = c->bpp_blocks[key];
+  if (blocks == 0 || c->bpp_smem[key] != smem) {
+    CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int per = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 32 + R, smem));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    blocks = std::max(1, per) * sms;
+    c->bpp_smem[key] = smem;
+    if (getenv("HPG_DEBUG")) fprintf(stderr, "bpp R=%d S=%d smem=%zu per_sm=%d\n", R, S, smem, per);
+  }
+  const int grid = (int)std::min<int64_t>(blocks, q.ntiles);
+  CUDA_TRY(launch_pdl_smem(c, fn, grid, 32 + R, smem, p, q, r, z));
+  ++c->launches;
+  return HPG_OK;
+}
+
+template <typename T>
+int gs_pass_bpp(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int rev) {
+  const int code = c->bpp_cfg[sizeof(T) == 4];
+#define HPG_BPP_CASE(TT, R, S)                                                        \
+  if (std::is_same<T, TT>::value && code == R * 10 + S)                                \
+    return gs_pass_bpp_t<TT, R, S>(c, L, col, (const TT*)r, (TT*)z, zero, rev);
+  HPG_BPP_CFGS(HPG_BPP_CASE)
+#undef HPG_BPP_CASE
+  return fail(HPG_E_ARG, "unknown pipelined brick configuration %d", code);
 }
 
 template <typename T>
@@ -936,10 +1002,14 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
       return rc;
     }
     if (c->tma_sweep) return gs_sweep_tma<T>(c, L, r, z, zero && c->known_zero);
-    const bool brick = brick_ok<T>(c, L, c->brick_cfg[sizeof(T) == 4] / 100);
+    const bool bpp = ((c->bpp >> (sizeof(T) == 4)) & 1) && brick_ok<T>(c, L, c->bpp_cfg[sizeof(T) == 4] / 10, true);
+    const bool brick = !bpp && brick_ok<T>(c, L, c->brick_cfg[sizeof(T) == 4] / 100);
     for (int col = 0; col < L.g.ncolors; ++col) {
       const int zz = zero && c->known_zero, rv = c->gs_rev && (col & 1);
-      if ((rc = brick ? gs_pass_brick<T>(c, L, col, r, z, zz, rv) : gs_pass_tma<T>(c, L, col, r, z, zz, rv))) return rc;
+      if ((rc = bpp     ? gs_pass_bpp<T>(c, L, col, r, z, zz, rv)
+                : brick ? gs_pass_brick<T>(c, L, col, r, z, zz, rv)
+                        : gs_pass_tma<T>(c, L, col, r, z, zz, rv)))
+        return rc;
     }
     return HPG_OK;
   }
@@ -2409,6 +2479,9 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   else if (!strcmp(key, "tma_cfg64")) c->tma_cfg[0] = (int)value;
   else if (!strcmp(key, "tma_cfg32")) c->tma_cfg[1] = (int)value;
   else if (!strcmp(key, "brick")) c->brick = (int)value;
+  else if (!strcmp(key, "bpp")) c->bpp = (int)value;
+  else if (!strcmp(key, "bpp_cfg64")) c->bpp_cfg[0] = (int)value;
+  else if (!strcmp(key, "bpp_cfg32")) c->bpp_cfg[1] = (int)value;
   else if (!strcmp(key, "spmv_tma")) c->spmv_tma = (int)value;
   else if (!strcmp(key, "spmv_cfg64")) c->spmv_cfg[0] = (int)value;
   else if (!strcmp(key, "spmv_cfg32")) c->spmv_cfg[1] = (int)value;
