@@ -112,8 +112,18 @@ __device__ __forceinline__ void cgs_fold(const double* partial, int cnt, double*
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool multi = ar.nranks > 1;
   for (int j = warp; j < cnt; j += kCgsWarps) {
+    // the same per-lane order as a plain strided loop (b = lane, lane + 32, ...), with
+    // eight loads in flight per lane instead of one L2 round trip per addend
     double a = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) a += __ldcg(partial + (int64_t)j * gridDim.x + b);
+    const double* row = partial + (int64_t)j * gridDim.x;
+    for (int b0 = lane; b0 < (int)gridDim.x; b0 += 32 * 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = b0 + 32 * u < (int)gridDim.x ? __ldcg(row + b0 + 32 * u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (b0 + 32 * u < (int)gridDim.x) a += v[u];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if (lane == 0) dst[j] = multi ? a : round_dot<T>(a, do_sqrt);

@@ -501,8 +501,15 @@ template <typename T>
 __global__ void k_fold(const T* __restrict__ partial, int nb, int kb, T* __restrict__ out, int do_sqrt) {
   if (kb == 1) {
     __shared__ T red[1024];
-    T a = T(0);
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) a += partial[b];
+    T a = T(0);  // per-thread order b = tid, tid + blockDim, ...; four loads in flight
+    for (int b0 = threadIdx.x; b0 < nb; b0 += 4 * blockDim.x) {
+      T v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = b0 + u * (int)blockDim.x < nb ? partial[b0 + u * blockDim.x] : T(0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (b0 + u * (int)blockDim.x < nb) a += v[u];
+    }
     red[threadIdx.x] = a;
     __syncthreads();
     for (int s = blockDim.x / 2; s > 0; s >>= 1) {
@@ -514,8 +521,16 @@ __global__ void k_fold(const T* __restrict__ partial, int nb, int kb, T* __restr
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int j = warp; j < kb; j += nw) {
-    T a = T(0);
-    for (int b = lane; b < nb; b += 32) a += partial[(int64_t)j * nb + b];
+    T a = T(0);  // per-lane order b = lane, lane + 32, ...; eight loads in flight
+    const T* row = partial + (int64_t)j * nb;
+    for (int b0 = lane; b0 < nb; b0 += 32 * 8) {
+      T v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = b0 + 32 * u < nb ? row[b0 + 32 * u] : T(0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (b0 + 32 * u < nb) a += v[u];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if (lane == 0) out[j] = a;
