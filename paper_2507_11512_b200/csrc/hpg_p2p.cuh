@@ -123,7 +123,10 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_halo_p2p(T* v, const int32_t* __restrict__ send_idx,
                                                   const __grid_constant__ P2PHalo h, uint64_t seq,
                                                   unsigned int* done) {
-  // launched with PDL: wait for the producer of v before packing it
+  // launched with PDL: let the consumer (the next colour pass / SpMV) launch now --
+  // it streams its matrix planes while the halo moves and waits for this grid
+  // before it reads v -- then wait for the producer of v before packing it
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int par = (int)(seq & 1);
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
