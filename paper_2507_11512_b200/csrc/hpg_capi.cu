@@ -267,7 +267,7 @@ struct hpg_ctx {
   // per-pass kernel (rows * 100 + CTAs per SM) [fp64, fp32]; measured 256^3 level-0 sweeps
   // (r02, tools/sweep_ab.py): fp32 64x16 479 us (256x5 with spills 699, 128x8 490),
   // fp64 64x10 776 us (128x6 897, 64x12 796) vs 581 / 1032 us for k_gs_pass / the wave sweep
-  int tma_cfg[2] = {3220, 6416};
+  int tma_cfg[2] = {3220, 12808};  // fp64 32x20; fp32 128x8 once face rows compute their columns (r02: sweep 440 -> 374 us, solve 2289 -> 2424 GF/s same box)
   // brick passes (hpg_brick.cuh): bit 0 fp64, bit 1 fp32; (rows * 100 + CTAs per SM).
   // Off: measured slower (r02, fp32 level-0 sweep 638 us at 128x8 vs 480 for the
   // tma pass) -- each CTA's neighbour-z boxes can only be requested after the PDL
@@ -1973,6 +1973,8 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
     if (tm) c->tma = atoi(tm);
     const char* fc = getenv("HPG_FACE_COLS");
     if (fc) c->face_cols = atoi(fc);
+    const char* t32 = getenv("HPG_TMA_CFG32");
+    if (t32) c->tma_cfg[1] = atoi(t32);
     const char* tr = getenv("HPG_TMA_MIN_ROWS");
     if (tr) c->tma_min_rows = atoll(tr);
     if (tma_setup<float>(c, sms) || tma_setup<double>(c, sms)) return bail(HPG_E_CUDA);
