@@ -28,7 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "HPG-MxP GFLOP/s (mixed, and speedup vs fp64) at 1/2/4/8 B200; % HBM roofline"
-GS_KERNEL = "k_gs_pass_tma<float,64,16> level-0 colour pass (multicolor GS, fp32; full and zero-guess sweeps)"
+GS_KERNEL = "k_gs_pass_tma<float,128,8> level-0 colour pass (multicolor GS, fp32; full and zero-guess sweeps)"
 UNIT = "GFLOP/s"
 
 
