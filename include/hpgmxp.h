@@ -184,6 +184,16 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
  *                reference forms and the flop model counts; default 0)
  *   "stencil"    1: rows whose 27 neighbours are local compute their columns in
  *                closed form instead of loading the index plane (default 1)
+ *   "tma"        bit mask (1 fp64, 2 fp32): colour passes of levels with >= "tma_min_rows"
+ *                rows stage their 27 value planes with one tensor copy (hpg_tma.cuh)
+ *   "tma_cfg32" / "tma_cfg64"  rows per CTA * 100 + CTAs per SM of that pass (12808 / 3220)
+ *   "spmv_tma"   bit mask: SpMV, fp64 residual and restriction with staged values;
+ *                "spmv_cfg32" / "spmv_cfg64" / "resid_cfg" / "restr_cfg32" / "restr_cfg64"
+ *   "face_cols"  bits: face rows off rank interfaces compute their columns (1 SpMV-type,
+ *                2 fp64 passes, 4 fp32 passes, 8 passes' x-face slot map, 16 SpMV x-face map)
+ *   "brick" / "bpp" / "tma_sweep"  experimental pass kernels (hpg_brick.cuh, the
+ *                persistent sweep); measured slower, off
+ *   "l2_window"  bytes of persisting L2 set-aside for z during the big passes (0: off)
  * Every option change drops the captured V-cycle graphs (re-captured on next use). */
 int hpg_set_option(hpg_ctx* ctx, const char* key, int64_t value);
 
