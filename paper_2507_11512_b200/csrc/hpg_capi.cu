@@ -243,6 +243,7 @@ struct hpg_ctx {
   double* pinned = nullptr;     // 256 host doubles
   int64_t launches = 0;
   bool cgs_fused = true;
+  int cgs_force = 0;  // option "cgs_cfg": force one fused-CGS2 configuration (tuning)
   bool general = false;  // some level uses an explicit (non-greedy) coloring
   bool graphs = true;    // replay captured V-cycles (single rank)
   // zero sweeps stream only the strictly-lower part (hpg_lower.cuh).  Off by
@@ -674,6 +675,7 @@ int gs_sweep_tma(hpg_ctx* c, Level& L, const T* r, T* z, int zero) {
 // per-pass TMA-fed colour pass: (rows per CTA, CTAs per SM) chosen per precision
 // by the option "tma_cfg32" / "tma_cfg64" = rows * 100 + CTAs per SM
 #define HPG_PASS_CFGS(X) X(float, 256, 5) X(float, 256, 4) X(float, 128, 10) X(float, 128, 8) X(float, 64, 16) X(float, 32, 32) \
+  X(float, 128, 6) X(float, 128, 7) X(float, 192, 5) X(float, 96, 10) X(double, 64, 6) X(double, 96, 6) \
   X(float, 64, 12) X(double, 128, 6) X(double, 128, 4) X(double, 64, 12) X(double, 64, 10) X(double, 64, 8) \
   X(double, 32, 20)
 template <typename T, int R>
@@ -1298,6 +1300,7 @@ int cgs2_passes(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
 // (WR, RPW, U) of the fused kernel per basis size: encoded WR*100 + RPW*10 + U
 // (RPW < 10).  HPG_CGS_CFG="kbmax:code,kbmax:code,..." overrides (tuning).
 int cgs_config(hpg_ctx* c, int kb) {
+  if (c->cgs_force > 0 && (c->cgs_force / 100) * ((c->cgs_force / 10) % 10) >= kb) return c->cgs_force;
   if (c->cgs_cfg.empty()) {
     const char* e = getenv("HPG_CGS_CFG");
     if (e) {
@@ -1309,7 +1312,8 @@ int cgs_config(hpg_ctx* c, int kb) {
       }
     }
     if (c->cgs_cfg.empty())
-      c->cgs_cfg = {{1, 118}, {2, 218}, {4, 418}, {8, 424}, {16, 442}, {24, 461}, {32, 481}, {64, 881}};
+      // r02 re-sweep (tools/cgs_sweep.py): kb 5-8 faster with 2 row groups x 4 rows (kb 6: 396 -> 354 us)
+      c->cgs_cfg = {{1, 118}, {2, 218}, {4, 418}, {8, 242}, {16, 442}, {24, 461}, {32, 481}, {64, 881}};
   }
   for (const auto& e : c->cgs_cfg)  // a configuration must hold all kb rows (WR * RPW >= kb)
     if (kb <= e.first && (e.second / 100) * ((e.second / 10) % 10) >= kb) return e.second;
@@ -2458,6 +2462,7 @@ static void drop_graphs(hpg_ctx* c) {
 int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(HPG_E_ARG, "null argument");
   if (!strcmp(key, "cgs_fused")) c->cgs_fused = value != 0;
+  else if (!strcmp(key, "cgs_cfg")) c->cgs_force = (int)value;
   else if (!strcmp(key, "pdl")) c->pdl = value != 0;
   else if (!strcmp(key, "overlap")) c->overlap = value != 0;
   else if (!strcmp(key, "p2p")) c->p2p = value != 0 && !c->peer_sym.empty();

@@ -461,7 +461,8 @@ def test_execution_variants_agree_bitwise():
     # really executed (checked through the eager launch counts), with graph
     # capture on and off
     ctx.set_option("graphs", 0)
-    variants = (("tma_min_rows", 0), ("bpp", 3), ("tail_rows", 1 << 30), ("tail_cluster", 16), ("tail_cluster", 8),
+    variants = (("tma_min_rows", 0), ("bpp", 3), ("bpp", 0), ("brick", 3), ("brick", 0), ("tma_sweep", 1),
+                ("tma_sweep", 0), ("tail_rows", 1 << 30), ("tail_cluster", 16), ("tail_cluster", 8),
                 ("gs_rev", 1), ("pdl", 0), ("known_zero", 0), ("face_cols", 0), ("wave", 0), ("lower", 1),
                 ("tma", 0))
     for graphs in (0, 1):
@@ -479,7 +480,7 @@ def test_execution_variants_agree_bitwise():
                 assert with_tail < without, (with_tail, without)
         for key, val in variants:  # back to the defaults for the next round
             ctx.set_option(key, {"tail_rows": 0, "tail_cluster": 0, "gs_rev": 0, "pdl": 1, "known_zero": 1,
-                                 "wave": 3, "lower": 0, "tma": 3, "tma_min_rows": 1 << 18, "face_cols": 31, "bpp": 0}[key])
+                                 "wave": 3, "lower": 0, "tma": 3, "tma_min_rows": 1 << 18, "face_cols": 31, "bpp": 0, "brick": 0, "tma_sweep": 0}[key])
     ctx.set_option("graphs", 1)
     ctx.set_option("known_zero", 1)
     ctx.set_option("known_zero", 1)
