@@ -244,6 +244,7 @@ struct hpg_ctx {
   int64_t launches = 0;
   bool cgs_fused = true;
   int cgs_force = 0;  // option "cgs_cfg": force one fused-CGS2 configuration (tuning)
+  int cgs_zigzag = 1;  // option "cgs_zigzag": CgsParams::zigzag of the fused CGS2 (r02: kb 30 -5%)
   bool general = false;  // some level uses an explicit (non-greedy) coloring
   bool graphs = true;    // replay captured V-cycles (single rank)
   // zero sweeps stream only the strictly-lower part (hpg_lower.cuh).  Off by
@@ -1234,6 +1235,7 @@ int cgs2_kb(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
 template <typename T, int WR, int RPW, int U>
 int cgs2_fused(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   hpg::CgsParams<T> p;
+  memset(&p, 0, sizeof p);
   p.Q = Q;
   p.w = w;
   p.qnext = qnext;
@@ -1242,6 +1244,7 @@ int cgs2_fused(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   p.ldq = ldq;
   p.n = c->lev[0].n;
   p.kb = kb;
+  p.zigzag = c->cgs_zigzag;
   p.ar = p2p_ar(c);
   p.seq0 = c->ar_seq + 1;
   if (c->nranks > 1) c->ar_seq += qnext ? 3 : 2;
@@ -2463,6 +2466,7 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(HPG_E_ARG, "null argument");
   if (!strcmp(key, "cgs_fused")) c->cgs_fused = value != 0;
   else if (!strcmp(key, "cgs_cfg")) c->cgs_force = (int)value;
+  else if (!strcmp(key, "cgs_zigzag")) c->cgs_zigzag = value != 0;
   else if (!strcmp(key, "pdl")) c->pdl = value != 0;
   else if (!strcmp(key, "overlap")) c->overlap = value != 0;
   else if (!strcmp(key, "p2p")) c->p2p = value != 0 && !c->peer_sym.empty();

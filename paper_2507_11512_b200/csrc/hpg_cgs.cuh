@@ -81,6 +81,8 @@ struct CgsParams {
   int kb;
   P2PAr ar;        // multi-rank: NVLink all-reduce between passes (ar.nranks == 1: none)
   uint64_t seq0;   // sequence number of the first of this call's all-reduces
+  int zigzag;      // passes B and D walk each CTA's range backwards, so they start on
+                   // the tiles passes A and C read last (still in L2)
 };
 
 #ifndef HPG_CGS_PIPE_MIN
@@ -274,7 +276,7 @@ struct CgsStream {
 // bases): software pipelined, the loads of iteration i+1 are in flight while
 // iteration i is consumed (two register sets, alternating); narrow bases use
 // one larger register set (U tiles) instead -- measured faster for kb <= 16.
-template <typename T, int WR, int RPW, int U, int MODE, bool PIPE>
+template <typename T, int WR, int RPW, int U, int MODE, bool PIPE, bool REV = false>
 __device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const double* h, double (&acc)[RPW],
                                          typename Vec16<T>::V* red) {
   using S = CgsStream<T, WR, RPW, U, MODE>;
@@ -284,22 +286,25 @@ __device__ __forceinline__ void cgs_pass(const CgsParams<T>& p, const double* h,
   const int64_t t0 = (int64_t)blockIdx.x * per;
   const int64_t t1 = t0 + per < ntiles ? t0 + per : ntiles;
   const S st(p, h, t1);
+  // iteration b covers tiles [at(b), at(b) + STEP); rev walks the range backwards
+  const int64_t nb = t1 > t0 ? (t1 - t0 + S::STEP - 1) / S::STEP : 0;
+  auto at = [&](int64_t b) { return t0 + (REV ? nb - 1 - b : b) * S::STEP; };
   if (!PIPE) {  // one register set: load, then consume
-    for (int64_t tb = t0; tb < t1; tb += S::STEP) {
+    for (int64_t b = 0; b < nb; ++b) {
       V q[U][RPW], wv[U];
-      st.load(tb, q, wv);
-      st.process(tb, q, wv, acc, red);
+      st.load(at(b), q, wv);
+      st.process(at(b), q, wv, acc, red);
     }
     return;
   }
   V qa[U][RPW], wa[U], qb[U][RPW], wb[U];
-  if (t0 < t1) st.load(t0, qa, wa);
-  for (int64_t tb = t0; tb < t1; tb += 2 * S::STEP) {
-    st.load(tb + S::STEP, qb, wb);
-    st.process(tb, qa, wa, acc, red);
-    if (tb + S::STEP >= t1) break;
-    st.load(tb + 2 * S::STEP, qa, wa);
-    st.process(tb + S::STEP, qb, wb, acc, red);
+  if (nb > 0) st.load(at(0), qa, wa);
+  for (int64_t b = 0; b < nb; b += 2) {
+    if (b + 1 < nb) st.load(at(b + 1), qb, wb);
+    st.process(at(b), qa, wa, acc, red);
+    if (b + 1 >= nb) break;
+    if (b + 2 < nb) st.load(at(b + 2), qa, wa);
+    st.process(at(b + 1), qb, wb, acc, red);
   }
 }
 
@@ -346,7 +351,8 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
     double acc[RPW];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) acc[r] = 0.0;
-    cgs_pass<T, WR, RPW, U, 1, (RPW >= HPG_CGS_PIPE_MIN)>(p, p.scal, acc, red);
+    if (p.zigzag) cgs_pass<T, WR, RPW, U, 1, (RPW >= HPG_CGS_PIPE_MIN), true>(p, p.scal, acc, red);
+    else cgs_pass<T, WR, RPW, U, 1, (RPW >= HPG_CGS_PIPE_MIN)>(p, p.scal, acc, red);
     cgs_store_rows<WR, RPW>(acc, p.kb, p.partial, sacc);
   }
   grid.sync();
@@ -368,6 +374,20 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
   constexpr int VN = Vec16<T>::N;
   const T bt = (T)__ldcg(p.scal + 128);
   const int64_t nv = p.n / VN;
+  if (p.zigzag) {
+    // this CTA's pass-C range, backwards (its last tiles are still in L2)
+    constexpr int TILE = 32 * VN;
+    const int64_t ntiles = (p.n + TILE - 1) / TILE, per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const int64_t v0 = (int64_t)blockIdx.x * per * 32, v1e = v0 + per * 32 < nv ? v0 + per * 32 : nv;
+    for (int64_t v = v1e - 1 - threadIdx.x; v >= v0; v -= blockDim.x) {
+      const VV x = __ldcg((const VV*)p.w + v);
+      VV y;
+#pragma unroll
+      for (int c = 0; c < VN; ++c) vset<T>(y, c, bt != T(0) ? div_rn(vget<T>(x, c), bt) : T(0));
+      ((VV*)p.qnext)[v] = y;
+    }
+    return;
+  }
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
     const VV x = __ldcg((const VV*)p.w + v);
     VV y;

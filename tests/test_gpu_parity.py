@@ -249,8 +249,10 @@ def test_fused_cgs2_matches_per_pass_kernels(dt, L):
     # every basis-size boundary of the fused kernel's (WR, RPW, U) table
     for k in (0, 1, 2, 3, 4, 7, 8, 12, 15, 16, 20, 23, 24, 29):
         outs = []
-        for fused in (1, 0):
+        # fused with the zigzag pass order (default), fused in one direction, per-pass kernels
+        for fused, zz in ((1, 1), (1, 0), (0, 0)):
             ctx.set_option("cgs_fused", fused)
+            ctx.set_option("cgs_zigzag", zz)
             ws = GmresWorkspace.allocate(n, 30, npdt, device="cuda")
             g = torch.Generator(device="cuda").manual_seed(k)
             ws.Q.copy_(torch.randn(ws.Q.shape, generator=g, device="cuda", dtype=tdt))
@@ -260,9 +262,11 @@ def test_fused_cgs2_matches_per_pass_kernels(dt, L):
                      _lib.ptr(ws.Q[k + 1]), res.ctypes.data_as(C.POINTER(C.c_double)))
             outs.append((res, ws.Q[k + 1].cpu().numpy()))
         # fp32 sums of random (non-orthogonal) rows cancel: scale the bound by the magnitudes
-        scale = tol * max(1.0, float(np.max(np.abs(outs[1][0]))))
-        np.testing.assert_allclose(outs[0][0], outs[1][0], rtol=tol, atol=scale)
-        np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=0, atol=tol)
+        scale = tol * max(1.0, float(np.max(np.abs(outs[2][0]))))
+        for o in outs[:2]:
+            np.testing.assert_allclose(o[0], outs[2][0], rtol=tol, atol=scale)
+            np.testing.assert_allclose(o[1], outs[2][1], rtol=0, atol=tol)
+    ctx.set_option("cgs_zigzag", 1)
     h.close()
 
 
