@@ -177,7 +177,7 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
  *   "gs_rev"     1: odd colors' passes walk their block backwards (L2 reuse at the turn)
  *   "spmv_ilv"   fp64 SpMV / residual CTAs interleaved over this many row segments
  *                (the color blocks) so x gathers hit L2 (default 4; bitwise identical)
- *   "spmv_ilv32" the same for the fp32 SpMV (default 1)
+ *   "spmv_ilv32" the same for the fp32 SpMV (default 8)
  *   "wave"       bit mask (1 fp64, 2 fp32): forward sweeps as one dataflow kernel
  *                (bitwise identical; default 1)
  *   "wave_min_rows" levels with fewer rows keep the per-color passes

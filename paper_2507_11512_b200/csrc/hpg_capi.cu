@@ -303,7 +303,7 @@ struct hpg_ctx {
   bool pdl = true;
   // SpMV CTA interleave over the color blocks [f64, f32] (HPG_SPMV_ILV, HPG_SPMV_ILV32);
   // measured 1xB200 256^3: f64 SpMV 760 -> 680 us at 4 (x is 134 MB, above L2), f32 454 -> 464 us at 4
-  int spmv_ilv[2] = {4, 1};
+  int spmv_ilv[2] = {4, 8};  // r02: fp32 8 (x gathers shared across the colour blocks in L2) -1.6% solve
   int gs_minb = 3;
   bool gs_rev = true;   // odd colors walk their block backwards (L2 reuse of z at the turn)
   bool stencil = true;  // interior rows compute their ELL columns instead of loading them
