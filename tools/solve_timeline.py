@@ -3,6 +3,7 @@ activity records): busy time per kernel, device idle gaps and what precedes
 them.  Tells whether the solve is kernel-bound or waits on the host.
 
     python tools/solve_timeline.py [--local 256] [--out gpurun_out/timeline.json]
+    torchrun --nproc-per-node N tools/solve_timeline.py   (one file per rank)
 """
 import argparse
 import collections
@@ -22,15 +23,23 @@ def main():
     import torch
     from torch.profiler import ProfilerActivity, profile
     from paper_2507_11512_b200.bench import BenchConfig, _build_state, _solve
+    from paper_2507_11512_b200.comm import World
     L = a.local
-    cfg = BenchConfig(local_nx=L, local_ny=L, local_nz=L, time_seconds=0)
-    hier, lv, b = _build_state(cfg, 1, None, 0)
+    nr = int(os.environ.get("WORLD_SIZE", "1"))
+    world = World() if nr > 1 else None
+    rank = world.rank if world else 0
+    cfg = BenchConfig(local_nx=L, local_ny=L, local_nz=L, ranks=nr, time_seconds=0)
+    hier, lv, b = _build_state(cfg, nr, world, rank)
     for _ in range(2):
-        _solve(cfg, hier, lv, b, None, 0, a.mode, cfg.tol, cfg.max_iters)
+        _solve(cfg, hier, lv, b, world, rank, a.mode, cfg.tol, cfg.max_iters)
     torch.cuda.synchronize()
+    if world:
+        world.barrier()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        res = _solve(cfg, hier, lv, b, None, 0, a.mode, cfg.tol, cfg.max_iters)
+        res = _solve(cfg, hier, lv, b, world, rank, a.mode, cfg.tol, cfg.max_iters)
         torch.cuda.synchronize()
+    if nr > 1:
+        a.out = a.out.replace(".json", f"_rank{rank}.json")
     ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     ks = sorted(((e.time_range.start, e.time_range.end, e.name) for e in ev), key=lambda x: x[0])
     busy = collections.defaultdict(float)
@@ -62,6 +71,8 @@ def main():
         "gaps_by_pair": sorted(([a1, b1, round(v[0], 1), v[1]] for (a1, b1), v in by_pair.items()),
                                key=lambda x: -x[2])[:25],
     }
+    # note: a PDL kernel's duration starts at its early launch (it waits on the device
+    # for its predecessor), so per-kernel sums over-count; span and idle are exact
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:
         json.dump(out, f, indent=1)
