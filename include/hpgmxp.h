@@ -168,7 +168,7 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
  *   "tail_cluster" > 0: that tail kernel runs as ONE cluster of this many CTAs (<= 16,
  *                hardware cluster barrier); 0: a cooperative grid (grid-wide barrier)
  *   "pdl"        1: stencil kernels use programmatic dependent launch
- *   "overlap"    1: multi-rank SpMV / GS overlap the halo exchange with interior rows
+ *   "overlap"    1: multi-rank SpMV / GS overlap the halo exchange with interior rows (default 1)
  *   "overlap_rows" only levels with at least this many rows overlap (default 2^20)
  *   "p2p"        1: NVLink peer-memory halo exchange + all-reduce (after hpg_p2p_open)
  *   "graphs"     1: single-rank V-cycles replay a captured CUDA graph per (prec, r, z)

@@ -221,7 +221,8 @@ struct hpg_ctx {
   cudaEvent_t ev_cgs = nullptr;             // (h1, h2, beta) landed in pinned memory
   int cgs_pending_kb = 0, cgs_pending_es = 4;
   bool cgs_pending_norm = false;
-  bool overlap = false;  // measured: no gain over the blocking exchange at 2 and 4 ranks
+  bool overlap = true;  // r02: with the tensor-copy kernels skipping the flagged rows, 4 ranks 706 -> 698 ms/solve
+  const uint8_t* pass_skip = nullptr;  // set around an overlapped tensor-copy launch (PassPlan/SpmvPlan::skip)
   // NVLink peer memory (hpg_p2p.cuh): symmetric buffer, peers' mappings, sequence numbers
   bool p2p = false;
   bool p2p_want = true;
@@ -244,6 +245,7 @@ struct hpg_ctx {
   int64_t launches = 0;
   bool cgs_fused = true;
   int cgs_force = 0;  // option "cgs_cfg": force one fused-CGS2 configuration (tuning)
+  bool overlap_tma = true;  // option "overlap_tma": overlapped levels keep the tensor-copy kernels
   int cgs_zigzag = 1;  // option "cgs_zigzag": CgsParams::zigzag of the fused CGS2 (r02: kb 30 -5%)
   bool general = false;  // some level uses an explicit (non-greedy) coloring
   bool graphs = true;    // replay captured V-cycles (single rank)
@@ -718,6 +720,7 @@ int gs_pass_tma_t(hpg_ctx* c, Level& L, int col, const T* r, T* z, int zero, int
   p.known0 = zero ? p.row0 : -1;
   p.rev = rev;
   p.color = col;
+  p.skip = c->pass_skip;
   p.st = stencil_of(c, L);
   if (p.st.on) {
     stencil_offsets(p.st, col, p.doff, &p.kmask);
@@ -991,7 +994,7 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
       if ((rc = gs_lower_launch<T>(c, L, col, r, z))) return rc;
     return HPG_OK;
   }
-  if (tma_ok<T>(c, L) && !(overlapped(c, l) && !zero)) {
+  if (tma_ok<T>(c, L) && !(overlapped(c, l) && !zero && !c->overlap_tma)) {
     if (zero) {
       if (L.n_ext > L.n) {  // zero initial guess: clear the halo tail; rows are all written
         CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n_ext - L.n, 4)), 256, z + L.n, L.n_ext - L.n));
@@ -1001,6 +1004,19 @@ int gs_sweep(hpg_ctx* c, int l, const T* r, T* z, int zero) {
         CUDA_TRY(launch_pdl(c, hpg::k_zero<T>, grid_for(cdiv(L.n, 4)), 256, z, L.n));
         ++c->launches;
       }
+    } else if (overlapped(c, l)) {
+      // the exchange runs on the halo stream while colour 0's rows that neither read
+      // a halo slot nor are sent run here; those rows follow once it has landed
+      if ((rc = exchange_begin(c, l, prec, z))) return rc;
+      c->pass_skip = L.hflag;
+      rc = gs_pass_tma<T>(c, L, 0, r, z, 0, 0);
+      c->pass_skip = nullptr;
+      if (rc) return rc;
+      if ((rc = exchange_end(c))) return rc;
+      if (L.nbnd0 && (rc = gs_pass_launch<T>(c, L, 0, L.nbnd0, r, z, nullptr, L.bnd0))) return rc;
+      for (int col = 1; col < L.g.ncolors; ++col)
+        if ((rc = gs_pass_tma<T>(c, L, col, r, z, 0, c->gs_rev && (col & 1)))) return rc;
+      return HPG_OK;
     } else if ((rc = do_exchange(c, l, prec, z))) {
       return rc;
     }
@@ -1737,6 +1753,7 @@ int spmv_tma_t(hpg_ctx* c, Level& L, const T* x, const T* b, T* y, double* parti
   }
   const int ilv = MODE == 2 ? 1 : std::max(1, c->spmv_ilv[sizeof(T) == 4]);
   p.ilv = ilv;
+  p.skip = MODE == 0 ? c->pass_skip : nullptr;
   if (rows >= 0) p.n = rows;  // MODE 2: the fine colour-0 rows
   const int64_t nbk = cdiv(p.n, R);
   if (nblocks) *nblocks = nbk;
@@ -1767,8 +1784,12 @@ bool spmv_tma_ok(hpg_ctx* c, const Level& L, int rows) {
 
 template <typename T>
 int spmv_launch(hpg_ctx* c, Level& L, int64_t cnt, const T* x, T* y, const uint8_t* skip, const int32_t* list) {
-  if (!skip && !list && cnt == L.n && spmv_tma_ok<T>(c, L, c->spmv_cfg[sizeof(T) == 4] / 100))
-    return spmv_tma<T, 0>(c, L, x, nullptr, y, nullptr, nullptr);
+  if ((!skip || c->overlap_tma) && !list && cnt == L.n && spmv_tma_ok<T>(c, L, c->spmv_cfg[sizeof(T) == 4] / 100)) {
+    c->pass_skip = skip;
+    const int rc = spmv_tma<T, 0>(c, L, x, nullptr, y, nullptr, nullptr);
+    c->pass_skip = nullptr;
+    return rc;
+  }
   if (skip || list)
     CUDA_TRY(launch_pdl(c, hpg::k_spmv<T, 0, true>, grid_for(cnt), 256, (const int32_t*)L.cols,
                         (const T*)vals_of<T>(L), L.ld, (int64_t)0, cnt, x, (const T*)nullptr, y, (double*)nullptr,
@@ -1936,7 +1957,9 @@ int hpg_create(hpg_ctx** out, int device, int rank, int nranks, const int proc_d
   } else if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
     return bail(fail(HPG_E_CUDA, "stream create failed"));
   }
-  if (cudaStreamCreateWithFlags(&c->halo, cudaStreamNonBlocking) != cudaSuccess ||
+  int prio_lo = 0, prio_hi = 0;  // the halo stream's CTAs are scheduled ahead of the compute stream's
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaStreamCreateWithPriority(&c->halo, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_cgs, cudaEventDisableTiming) != cudaSuccess)
@@ -2466,6 +2489,7 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return fail(HPG_E_ARG, "null argument");
   if (!strcmp(key, "cgs_fused")) c->cgs_fused = value != 0;
   else if (!strcmp(key, "cgs_cfg")) c->cgs_force = (int)value;
+  else if (!strcmp(key, "overlap_tma")) c->overlap_tma = value != 0;
   else if (!strcmp(key, "cgs_zigzag")) c->cgs_zigzag = value != 0;
   else if (!strcmp(key, "pdl")) c->pdl = value != 0;
   else if (!strcmp(key, "overlap")) c->overlap = value != 0;

@@ -396,6 +396,8 @@ struct PassPlan {
   uint32_t kmask;       // implicit-index rows: slot s's load skipped when bit s is set
   int32_t doff[27];     // implicit-index rows: slot s gathers column i + doff[s]
   int xface;            // x-face rows use the compile-time slot map (st_xface)
+  const uint8_t* skip;  // overlapped exchange: face rows flagged here are left to a later
+                        // launch (they read halo slots / are sent); interior rows never are
   Stencil st;
 };
 
@@ -437,6 +439,10 @@ __global__ void __launch_bounds__(ROWS, MINB) k_gs_pass_tma(const __grid_constan
       acc = add_rn(acc, mul_rn(vs, g[s]));
     }
   } else {
+    if (p.skip && p.skip[i]) {
+      mbar_wait(bar, 0);  // (the tile's copy must land before the CTA may retire)
+      return;
+    }
     int32_t c[27];
     const int xf = (p.st.on && p.xface) ? st_xface(p.st, i, p.color) : 0;
     if (xf) {  // x-face row: compile-time slot map per side
@@ -490,6 +496,7 @@ struct SpmvPlan {
   int ilv;
   int xface;            // x-face rows use the compile-time slot map (st_xface)
   int32_t doff[8][27];  // implicit-index rows of colour c: slot s reads column i + doff[c][s]
+  const uint8_t* skip;  // MODE 0, overlapped exchange: flagged (face) rows are left to a later launch
   Stencil st;
 };
 
@@ -519,6 +526,7 @@ __global__ void __launch_bounds__(ROWS, MINB) k_spmv_tma(const __grid_constant__
   const int t = threadIdx.x;
   const int64_t i = tile0 + t;
   double sq = 0.0;
+  bool skipped = false;
   if (i < p.n) {
     T g[27];
     const int col = p.st.on ? (int)(tile0 / p.n8) : 0;
@@ -527,6 +535,7 @@ __global__ void __launch_bounds__(ROWS, MINB) k_spmv_tma(const __grid_constant__
 #pragma unroll
       for (int s = 0; s < 27; ++s) g[s] = xi[p.doff[col][s]];
     } else {
+      skipped = MODE == 0 && p.skip && p.skip[i];
       int32_t cf[27];
       const int xf = (p.st.on && p.xface) ? st_xface(p.st, i, col) : 0;
       if (xf) {  // x-face row: compile-time slot map per side
@@ -551,7 +560,7 @@ __global__ void __launch_bounds__(ROWS, MINB) k_spmv_tma(const __grid_constant__
 #pragma unroll
     for (int s = 0; s < 27; ++s) acc = add_rn(acc, mul_rn(sv[s * ROWS + t], g[s]));
     if (MODE == 0) {
-      y[i] = acc;
+      if (!skipped) y[i] = acc;
     } else if (MODE == 2) {
       y[dst[i]] = sub_rn(b[i], acc);
     } else {

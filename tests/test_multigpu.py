@@ -95,7 +95,9 @@ def test_two_ranks_x_split_nccl_path():
 
 @pytest.mark.skipif(_gpus() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("env", [{"HPG_P2P": "0"}, {"HPG_OVERLAP": "1"}, {"HPG_P2P": "0", "HPG_OVERLAP": "1"},
-                                 {"HPG_CGS_FUSED": "0"}, {"HPG_NCCL": "0"}])
+                                 {"HPG_CGS_FUSED": "0"}, {"HPG_NCCL": "0"},
+                                 # the overlapped exchange under the tensor-copy pass / SpMV (skip flags)
+                                 {"HPG_OVERLAP": "1", "HPG_OVERLAP_ROWS": "0", "HPG_TMA_MIN_ROWS": "0"}])
 def test_two_ranks_alternative_paths(env):
     """NCCL data path, overlapped exchange, per-pass CGS2 and the P2P-only
     context (no NCCL communicator): same bitwise kernels, converged solves."""
