@@ -169,7 +169,7 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
  *                hardware cluster barrier); 0: a cooperative grid (grid-wide barrier)
  *   "pdl"        1: stencil kernels use programmatic dependent launch
  *   "overlap"    1: multi-rank SpMV / GS overlap the halo exchange with interior rows (default 1)
- *   "overlap_rows" only levels with at least this many rows overlap (default 2^20)
+ *   "overlap_rows" only levels with at least this many rows overlap (default 0: all)
  *   "p2p"        1: NVLink peer-memory halo exchange + all-reduce (after hpg_p2p_open)
  *   "graphs"     1: single-rank V-cycles replay a captured CUDA graph per (prec, r, z)
  *   "known_zero" 1: zero-initial-guess sweeps skip the loads of not-yet-updated colors

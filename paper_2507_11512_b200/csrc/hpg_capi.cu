@@ -233,7 +233,7 @@ struct hpg_ctx {
   unsigned int* done = nullptr;
   uint64_t halo_seq = 0, ar_seq = 0;
   std::vector<std::pair<int, int>> cgs_cfg;  // (kb max, WR*100 + RPW*10 + U)
-  int64_t overlap_rows = 1 << 20;  // only levels this large hide an exchange behind interior rows
+  int64_t overlap_rows = 0;  // only levels this large hide an exchange behind interior rows (r02: all, 4 ranks -1 ms)
   ncclComm_t comm = nullptr;
   int nb = 0;                   // reduction grid
   void* partial = nullptr;      // nb * 64 elements (f64-sized)
