@@ -164,6 +164,8 @@ int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
  *   "cgs_fused"  1: CGS2 as one cooperative kernel (single rank, or NVLink peers), 0: per-pass kernels
  *   "cgs_cfg"    force one (row groups, rows per warp, tiles) configuration of that kernel
  *   "cgs_zigzag" 1: its passes B and D walk each CTA's range backwards (L2 reuse; default 1)
+ *   "cgs_solo"   1: single rank, every CTA folds the dot partials itself (one grid barrier
+ *                per fold instead of two; bitwise the same values; default 1)
  *   "tail_rows"  levels with at most this many rows run in the persistent V-cycle tail kernel
  *   "tail_cluster" > 0: that tail kernel runs as ONE cluster of this many CTAs (<= 16,
  *                hardware cluster barrier); 0: a cooperative grid (grid-wide barrier)

@@ -246,6 +246,7 @@ struct hpg_ctx {
   bool cgs_fused = true;
   int cgs_force = 0;  // option "cgs_cfg": force one fused-CGS2 configuration (tuning)
   bool overlap_tma = true;  // option "overlap_tma": overlapped levels keep the tensor-copy kernels
+  int cgs_solo = 1;    // option "cgs_solo": CgsParams::solo_fold
   int cgs_zigzag = 1;  // option "cgs_zigzag": CgsParams::zigzag of the fused CGS2 (r02: kb 30 -5%)
   bool general = false;  // some level uses an explicit (non-greedy) coloring
   bool graphs = true;    // replay captured V-cycles (single rank)
@@ -1261,6 +1262,7 @@ int cgs2_fused(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   p.n = c->lev[0].n;
   p.kb = kb;
   p.zigzag = c->cgs_zigzag;
+  p.solo_fold = c->cgs_solo;
   p.ar = p2p_ar(c);
   p.seq0 = c->ar_seq + 1;
   if (c->nranks > 1) c->ar_seq += qnext ? 3 : 2;
@@ -2490,6 +2492,7 @@ int hpg_set_option(hpg_ctx* c, const char* key, int64_t value) {
   if (!strcmp(key, "cgs_fused")) c->cgs_fused = value != 0;
   else if (!strcmp(key, "cgs_cfg")) c->cgs_force = (int)value;
   else if (!strcmp(key, "overlap_tma")) c->overlap_tma = value != 0;
+  else if (!strcmp(key, "cgs_solo")) c->cgs_solo = value != 0;
   else if (!strcmp(key, "cgs_zigzag")) c->cgs_zigzag = value != 0;
   else if (!strcmp(key, "pdl")) c->pdl = value != 0;
   else if (!strcmp(key, "overlap")) c->overlap = value != 0;

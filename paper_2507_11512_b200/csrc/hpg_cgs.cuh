@@ -83,6 +83,7 @@ struct CgsParams {
   uint64_t seq0;   // sequence number of the first of this call's all-reduces
   int zigzag;      // passes B and D walk each CTA's range backwards, so they start on
                    // the tiles passes A and C read last (still in L2)
+  int solo_fold;   // single rank: every CTA folds the partials (one grid barrier per fold)
 };
 
 #ifndef HPG_CGS_PIPE_MIN
@@ -137,6 +138,35 @@ __device__ __forceinline__ void cgs_fold(const double* partial, int cnt, double*
   }
 }
 
+// Single rank: EVERY CTA folds the partials itself, in cgs_fold's order (so the
+// values are bitwise the same), into shared memory -- one grid barrier per
+// fold instead of two; CTA 0 also stores them to gdst for the host.
+template <typename T>
+__device__ __forceinline__ void cta_fold(const double* partial, int cnt, double* sh, bool do_sqrt, double* gdst) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < cnt; j += kCgsWarps) {
+    double a = 0.0;
+    const double* row = partial + (int64_t)j * gridDim.x;
+    for (int b0 = lane; b0 < (int)gridDim.x; b0 += 32 * 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = b0 + 32 * u < (int)gridDim.x ? __ldcg(row + b0 + 32 * u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (b0 + 32 * u < (int)gridDim.x) a += v[u];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) {
+      const double v = round_dot<T>(a, do_sqrt);
+      sh[j] = v;
+      if (gdst) gdst[j] = v;
+    }
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ double ld_h(const double* a) { return __isShared(a) ? *a : __ldcg(a); }
+
 // Warp roles: WR warps split the rows (row group rg = warp % WR streams rows
 // rg, rg+WR, ...), WE = W/WR element groups split the tiles, so small bases
 // still keep every warp streaming.
@@ -166,7 +196,7 @@ struct CgsStream {
 #pragma unroll
     for (int r = 0; r < RPW; ++r) {
       const int j = rg + r * WR;
-      hr[r] = (MODE > 0 && j < kb) ? (T)__ldcg(h + j) : T(0);
+      hr[r] = (MODE > 0 && j < kb) ? (T)ld_h(h + j) : T(0);
     }
   }
 
@@ -337,6 +367,21 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
   cg::grid_group grid = cg::this_grid();
   __shared__ V red[WR > 1 ? U * kCgsWarps * 32 : 1];
   __shared__ double sacc[kCgsWarps * RPW];
+  // single rank: redundant per-CTA folds (cta_fold); pass B's partials go to a second
+  // buffer so no CTA overwrites partials another CTA may still be folding
+  __shared__ double hsh[64];
+  const bool solo = p.ar.nranks <= 1 && p.solo_fold;
+  double* part_b = solo ? p.partial + (int64_t)64 * gridDim.x : p.partial;
+  auto fold = [&](const double* part, int cnt, int slot, bool sq, uint64_t seq) -> const double* {
+    grid.sync();
+    if (solo) {
+      cta_fold<T>(part, cnt, hsh, sq, blockIdx.x == 0 ? p.scal + slot : nullptr);
+      return hsh;
+    }
+    cgs_fold<T>(part, cnt, p.scal + slot, sq, p.ar, seq);
+    grid.sync();
+    return p.scal + slot;
+  };
   {  // pass A: h1
     double acc[RPW];
 #pragma unroll
@@ -344,35 +389,29 @@ __global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_cons
     cgs_pass<T, WR, RPW, U, 0, (RPW >= HPG_CGS_PIPE_MIN)>(p, nullptr, acc, red);
     cgs_store_rows<WR, RPW>(acc, p.kb, p.partial, sacc);
   }
-  grid.sync();
-  cgs_fold<T>(p.partial, p.kb, p.scal, false, p.ar, p.seq0);
-  grid.sync();
+  const double* h1 = fold(p.partial, p.kb, 0, false, p.seq0);
   {  // pass B: w -= Q^T h1 ; h2
     double acc[RPW];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) acc[r] = 0.0;
-    if (p.zigzag) cgs_pass<T, WR, RPW, U, 1, (RPW >= HPG_CGS_PIPE_MIN), true>(p, p.scal, acc, red);
-    else cgs_pass<T, WR, RPW, U, 1, (RPW >= HPG_CGS_PIPE_MIN)>(p, p.scal, acc, red);
-    cgs_store_rows<WR, RPW>(acc, p.kb, p.partial, sacc);
+    if (p.zigzag) cgs_pass<T, WR, RPW, U, 1, (RPW >= HPG_CGS_PIPE_MIN), true>(p, h1, acc, red);
+    else cgs_pass<T, WR, RPW, U, 1, (RPW >= HPG_CGS_PIPE_MIN)>(p, h1, acc, red);
+    cgs_store_rows<WR, RPW>(acc, p.kb, part_b, sacc);
   }
-  grid.sync();
-  cgs_fold<T>(p.partial, p.kb, p.scal + 64, false, p.ar, p.seq0 + 1);
-  grid.sync();
+  const double* h2 = fold(part_b, p.kb, 64, false, p.seq0 + 1);
   {  // pass C: w -= Q^T h2 ; beta^2 (row-group-0 warps hold the block's share)
     double acc[RPW];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) acc[r] = 0.0;
-    cgs_pass<T, WR, RPW, U, 2, (RPW >= HPG_CGS_PIPE_MIN)>(p, p.scal + 64, acc, red);
+    cgs_pass<T, WR, RPW, U, 2, (RPW >= HPG_CGS_PIPE_MIN)>(p, h2, acc, red);
     cgs_store_rows<WR, RPW>(acc, 1, p.partial, sacc);
   }
   if (p.qnext == nullptr) return;
-  grid.sync();
-  cgs_fold<T>(p.partial, 1, p.scal + 128, true, p.ar, p.seq0 + 2);
-  grid.sync();
+  const double* bsq = fold(p.partial, 1, 128, true, p.seq0 + 2);
   // pass D: Q[k+1] = w / beta  (ref: krylov.py:269-273), 16-byte vectors
   using VV = typename Vec16<T>::V;
   constexpr int VN = Vec16<T>::N;
-  const T bt = (T)__ldcg(p.scal + 128);
+  const T bt = (T)ld_h(bsq);
   const int64_t nv = p.n / VN;
   if (p.zigzag) {
     // this CTA's pass-C range, backwards (its last tiles are still in L2)
