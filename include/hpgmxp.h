@@ -162,7 +162,8 @@ int64_t hpg_launch_count(hpg_ctx* ctx);
 int hpg_timers(hpg_ctx* ctx, int mode, double* seconds);
 /* Tuning switches (results are identical up to reduction order):
  *   "cgs_fused"  1: CGS2 as one cooperative kernel (single rank, or NVLink peers), 0: per-pass kernels
- *   "cgs_cfg"    force one (row groups, rows per warp, tiles) configuration of that kernel
+ *   "cgs_cfg"    force one configuration of that kernel: [CTAs per SM * 1000 +] row groups * 100
+ *                + rows per warp * 10 + tiles (e.g. 481, 3441)
  *   "cgs_zigzag" 1: its passes B and D walk each CTA's range backwards (L2 reuse; default 1)
  *   "cgs_solo"   1: single rank, every CTA folds the dot partials itself (one grid barrier
  *                per fold instead of two; bitwise the same values; default 1)

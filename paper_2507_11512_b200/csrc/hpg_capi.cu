@@ -1249,7 +1249,7 @@ int cgs2_kb(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
 }
 
 // single-rank CGS2: one cooperative launch (csrc/hpg_cgs.cuh)
-template <typename T, int WR, int RPW, int U>
+template <typename T, int WR, int RPW, int U, int MINB = 2>
 int cgs2_fused(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   hpg::CgsParams<T> p;
   memset(&p, 0, sizeof p);
@@ -1267,7 +1267,7 @@ int cgs2_fused(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
   p.seq0 = c->ar_seq + 1;
   if (c->nranks > 1) c->ar_seq += qnext ? 3 : 2;
   if (ldq % 32) return fail(HPG_E_ARG, "basis row stride must be a multiple of 32 elements");
-  auto fn = hpg::k_cgs2_fused<T, WR, RPW, U>;
+  auto fn = hpg::k_cgs2_fused<T, WR, RPW, U, MINB>;
   int per = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, hpg::kCgsThreads, 0));
   int sms = 148;
@@ -1321,7 +1321,8 @@ int cgs2_passes(hpg_ctx* c, T* Q, int64_t ldq, int kb, T* w, T* qnext) {
 // (WR, RPW, U) of the fused kernel per basis size: encoded WR*100 + RPW*10 + U
 // (RPW < 10).  HPG_CGS_CFG="kbmax:code,kbmax:code,..." overrides (tuning).
 int cgs_config(hpg_ctx* c, int kb) {
-  if (c->cgs_force > 0 && (c->cgs_force / 100) * ((c->cgs_force / 10) % 10) >= kb) return c->cgs_force;
+  // code: [MINB * 1000 +] WR * 100 + RPW * 10 + U (MINB: CTAs per SM the kernel is built for, default 2)
+  if (c->cgs_force > 0 && ((c->cgs_force % 1000) / 100) * ((c->cgs_force / 10) % 10) >= kb) return c->cgs_force;
   if (c->cgs_cfg.empty()) {
     const char* e = getenv("HPG_CGS_CFG");
     if (e) {
@@ -1333,11 +1334,13 @@ int cgs_config(hpg_ctx* c, int kb) {
       }
     }
     if (c->cgs_cfg.empty())
-      // r02 re-sweep (tools/cgs_sweep.py): kb 5-8 faster with 2 row groups x 4 rows (kb 6: 396 -> 354 us)
-      c->cgs_cfg = {{1, 118}, {2, 218}, {4, 418}, {8, 242}, {16, 442}, {24, 461}, {32, 481}, {64, 881}};
+      // r02 re-sweeps (tools/cgs_sweep.py): kb 5-8 with 2 row groups x 4 rows (kb 6: 396 -> 354 us);
+      // kb 9-14 with 2 x 8 rows (kb 12: 579 -> 549 us); kb 15-16 with 4 x 4 rows built for 3 CTAs
+      // per SM (kb 16: 677 -> 643 us)
+      c->cgs_cfg = {{1, 118}, {2, 218}, {4, 418}, {8, 242}, {14, 281}, {16, 3441}, {24, 461}, {32, 481}, {64, 881}};
   }
   for (const auto& e : c->cgs_cfg)  // a configuration must hold all kb rows (WR * RPW >= kb)
-    if (kb <= e.first && (e.second / 100) * ((e.second / 10) % 10) >= kb) return e.second;
+    if (kb <= e.first && ((e.second % 1000) / 100) * ((e.second / 10) % 10) >= kb) return e.second;
   return 881;
 }
 
@@ -1366,6 +1369,15 @@ int cgs2_fused_dispatch(hpg_ctx* c, int code, T* Q, int64_t ldq, int kb, T* w, T
     HPG_CGS_CASE(4, 8, 1)
     HPG_CGS_CASE(8, 8, 1)
 #undef HPG_CGS_CASE
+#define HPG_CGS3_CASE(WR, RPW, U)        \
+  case 3000 + WR * 100 + RPW * 10 + U:  \
+    return cgs2_fused<T, WR, RPW, U, 3>(c, Q, ldq, kb, w, qnext);
+    HPG_CGS3_CASE(4, 4, 1)
+    HPG_CGS3_CASE(8, 4, 1)
+    HPG_CGS3_CASE(8, 3, 1)
+    HPG_CGS3_CASE(4, 2, 2)
+    HPG_CGS3_CASE(8, 2, 2)
+#undef HPG_CGS3_CASE
   }
   return fail(HPG_E_ARG, "unknown CGS2 configuration %d", code);
 }

@@ -360,8 +360,8 @@ __device__ __forceinline__ void cgs_store_rows(const double (&acc)[RPW], int kb,
   __syncthreads();
 }
 
-template <typename T, int WR, int RPW, int U>
-__global__ void __launch_bounds__(kCgsThreads, 2) k_cgs2_fused(const __grid_constant__ CgsParams<T> p) {
+template <typename T, int WR, int RPW, int U, int MINB = 2>
+__global__ void __launch_bounds__(kCgsThreads, MINB) k_cgs2_fused(const __grid_constant__ CgsParams<T> p) {
   namespace cg = cooperative_groups;
   using V = typename Vec16<T>::V;
   cg::grid_group grid = cg::this_grid();

@@ -8,7 +8,8 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-CODES = [118, 218, 418, 818, 424, 824, 422, 432, 832, 442, 842, 441, 242, 281, 461, 861, 481, 881]
+CODES = [int(c) for c in os.environ["CGS_CODES"].split(",")] if os.environ.get("CGS_CODES") else [118, 218, 418, 818, 424, 824, 422, 432, 832, 442, 842, 441, 242, 281, 461, 861, 481, 881,
+         3441, 3841, 3831, 3422, 3822]  # 3xxx: built for 3 CTAs per SM
 
 
 def main():
@@ -30,10 +31,11 @@ def main():
     res = np.zeros(64)
     st = ctx.stream
     out = {}
-    for kb in (1, 2, 4, 6, 8, 12, 16, 20, 24, 28, 30):
+    kbs = [int(x) for x in os.environ.get("CGS_KBS", "1,2,4,6,8,12,16,20,24,28,30").split(",")]
+    for kb in kbs:
         row = {}
         for code in [0] + CODES:
-            wr, rpw = code // 100, (code // 10) % 10
+            wr, rpw = (code % 1000) // 100, (code // 10) % 10
             if code and wr * rpw < kb:
                 continue
             ctx.set_option("cgs_cfg", code)
@@ -51,6 +53,8 @@ def main():
             row[code] = round(e0.elapsed_time(e1) / 5 * 1e3, 1)
         best = min((v, c) for c, v in row.items() if c)
         out[kb] = {"table": row[0], "best": best[1], "best_us": best[0]}
+        if os.environ.get("CGS_ROWS"):
+            out[kb]["all"] = row
         print(kb, out[kb], flush=True)
     print(json.dumps(out))
     hier.close()
