@@ -114,22 +114,37 @@ __device__ __forceinline__ void cgs_fold(const double* partial, int cnt, double*
   if (blockIdx.x != 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool multi = ar.nranks > 1;
-  for (int j = warp; j < cnt; j += kCgsWarps) {
-    // the same per-lane order as a plain strided loop (b = lane, lane + 32, ...), with
-    // eight loads in flight per lane instead of one L2 round trip per addend
-    double a = 0.0;
-    const double* row = partial + (int64_t)j * gridDim.x;
-    for (int b0 = lane; b0 < (int)gridDim.x; b0 += 32 * 8) {
-      double v[8];
+  // the same per-lane order as a plain strided loop (b = lane, lane + 32, ...); two rows
+  // per warp and ten partials per lane in flight at once (one L2 round trip per 320)
+  constexpr int RW = 2, UL = 10;
+  const int G = (int)gridDim.x;
+  for (int j0 = warp; j0 < cnt; j0 += kCgsWarps * RW) {
+    double a[RW];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = b0 + 32 * u < (int)gridDim.x ? __ldcg(row + b0 + 32 * u) : 0.0;
+    for (int r = 0; r < RW; ++r) a[r] = 0.0;
+    for (int b0 = lane; b0 < G; b0 += 32 * UL) {
+      double v[RW][UL];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (b0 + 32 * u < (int)gridDim.x) a += v[u];
+      for (int r = 0; r < RW; ++r) {
+        const int j = j0 + r * kCgsWarps;
+        const double* row = partial + (int64_t)j * G;
+#pragma unroll
+        for (int u = 0; u < UL; ++u) v[r][u] = (j < cnt && b0 + 32 * u < G) ? __ldcg(row + b0 + 32 * u) : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < RW; ++r)
+#pragma unroll
+        for (int u = 0; u < UL; ++u)
+          if (b0 + 32 * u < G) a[r] += v[r][u];
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) dst[j] = multi ? a : round_dot<T>(a, do_sqrt);
+    for (int r = 0; r < RW; ++r) {
+      double x = a[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      const int j = j0 + r * kCgsWarps;
+      if (lane == 0 && j < cnt) dst[j] = multi ? x : round_dot<T>(x, do_sqrt);
+    }
   }
   if (multi) {
     __syncthreads();
